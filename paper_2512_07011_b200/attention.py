@@ -1,0 +1,228 @@
+"""BSFA forward on sm_100a: the batched entry point and the reference drop-in.
+
+* :func:`attention` -- batched/GQA entry point on CUDA tensors
+  (q [B, Hq, N, d], k/v [B, Hkv, N, d], bf16).  One launch of the
+  ``bsfa_fwd`` C-ABI kernel; returns O (bf16), LSE (fp32) and optionally the
+  per-tile decision trace and kept/skipped/V-load counters.
+* :func:`flash_forward` -- the reference signature
+  ``flash_forward(inp, tiles, gate, ctx=None, threads=1, inject_fault=False)
+  -> (AttentionOutput, GateTrace)`` (reference engine.py:117-193), numpy in,
+  numpy out, one head, executed by the same kernel.
+
+Semantics kept from the reference engine:
+  - sequences are padded to lcm(b_m, b_n) by repeating the last row
+    (engine.py:99-114) and outputs sliced back to the valid length;
+  - frontier tiles are always processed with the element-wise causal mask,
+    off-frontier tiles go through the gate (engine.py:157-175);
+  - keep iff max(QK^T * scale over the tile) > T, strictly (gates.py:77-78);
+  - scale = float32(1/sqrt(d)) (engine.py:144); LSE = m + ln(l) in scaled
+    natural-log units (engine.py:182);
+  - a row with a non-finite accumulator or l <= 0 raises NumericError
+    (engine.py:178-179) when ``check_numerics`` is on (always on in the
+    drop-in, which synchronises anyway).
+Numerics differ by design: inputs are rounded to bf16, P is bf16 on the
+tensor cores, O is emitted in bf16 (tolerance documented in DESIGN.md).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import AttentionOutput, HeadInput
+from .errors import ConfigurationError, InvalidInputError, NumericError
+from .gates import GateContext, ThresholdGate, kernel_gate_mode
+from .thresholds import ThresholdTensor
+from .tiling import TileConfig, require_kernel_tiles
+from .trace import GateTrace
+
+
+@dataclass
+class AttentionResult:
+    o: torch.Tensor                  # [B, Hq, N, d] bf16
+    lse: torch.Tensor                # [B, Hq, N] fp32
+    decisions: torch.Tensor | None   # [B, Hq, M_q, M_kv] int8 (padded grid) or None
+    counters: torch.Tensor           # int64 [3]: reachable, kept, V tiles loaded
+    status: torch.Tensor             # int32 [1]; non-zero = numeric failure
+
+
+def _scale_for(d: int) -> float:
+    return float(np.float32(1.0) / np.sqrt(np.float32(d)))
+
+
+def reference_scale(d: int) -> float:
+    """float32(1/sqrt(d)) exactly as reference engine.py:144 computes it."""
+    return float(np.float32(1.0 / np.sqrt(d)))
+
+
+def _pad_rows(x: torch.Tensor, target: int) -> torch.Tensor:
+    n = x.shape[2]
+    if n == target:
+        return x
+    tail = x[:, :, n - 1:n, :].expand(-1, -1, target - n, -1)
+    return torch.cat([x, tail], dim=2)
+
+
+def _pad_dim(x: torch.Tensor, dp: int) -> torch.Tensor:
+    d = x.shape[3]
+    if d == dp:
+        return x
+    return torch.nn.functional.pad(x, (0, dp - d))
+
+
+def _check_inputs(q, k, v):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(t, torch.Tensor):
+            raise InvalidInputError(f"{name} must be a torch tensor")
+        if t.dim() != 4:
+            raise InvalidInputError(f"{name} must be 4-D [B, H, N, d], got {tuple(t.shape)}")
+        if not t.is_cuda:
+            raise InvalidInputError(f"{name} must be on a CUDA device (no CPU fallback)")
+    if k.shape != v.shape:
+        raise InvalidInputError(f"k/v shapes differ: {tuple(k.shape)} vs {tuple(v.shape)}")
+    b, hq, n, d = q.shape
+    if k.shape[0] != b or k.shape[2] != n or k.shape[3] != d:
+        raise InvalidInputError(f"q {tuple(q.shape)} and k {tuple(k.shape)} disagree")
+    hkv = k.shape[1]
+    if hkv < 1 or hq % hkv:
+        raise InvalidInputError(f"query heads {hq} must be a multiple of kv heads {hkv}")
+    if n < 1 or d < 1:
+        raise InvalidInputError("empty sequence or head dimension")
+    if d > 128:
+        raise InvalidInputError(f"head_dim {d} > 128 is not supported by the kernel")
+
+
+def _as_kernel_operand(x: torch.Tensor, n_pad: int, d_pad: int) -> torch.Tensor:
+    x = x.to(torch.bfloat16)
+    x = _pad_dim(_pad_rows(x, n_pad), d_pad)
+    if x.stride(3) != 1 or (x.stride(2) * 2) % 16 or x.data_ptr() % 16:
+        x = x.contiguous()
+    return x
+
+
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = True,
+              gate=None, thresholds: ThresholdTensor | None = None, layer: int = 0,
+              k_level: int | None = None, head_offset: int = 0,
+              tiles: TileConfig = TileConfig(), return_trace: bool = False,
+              inject_fault: bool = False, check_numerics: bool = False,
+              scale: float | None = None) -> AttentionResult:
+    """Block-sparse (or dense) causal/non-causal GQA attention forward.
+
+    Gate selection: ``thresholds`` + ``k_level`` (+ ``layer``) runs the
+    ThresholdGate with per-(head, query block) thresholds
+    ``values[level, layer, head_offset + h, min(i, P-1)]``; otherwise ``gate``
+    may be a DenseGate / FrontierOnlyGate / ThresholdGate object; with
+    neither the run is dense.
+    """
+    _check_inputs(q, k, v)
+    require_kernel_tiles(tiles)
+    bsz, hq, n, d = q.shape
+    hkv = k.shape[1]
+
+    thr_dev = None
+    thr_positions = 0
+    if thresholds is None and isinstance(gate, ThresholdGate):
+        thresholds = gate.tensor
+    if thresholds is not None:
+        ThresholdGate(thresholds).validate(tiles, GateContext(layer=layer, k_level=k_level))
+        thresholds.check_site(layer, head_offset)
+        if head_offset + hq > thresholds.num_heads:
+            raise ConfigurationError(
+                f"heads [{head_offset}, {head_offset + hq}) outside calibrated {thresholds.num_heads}")
+        sl = thresholds.layer_slice(k_level, layer)[head_offset:head_offset + hq]
+        thr_dev = torch.from_numpy(np.ascontiguousarray(sl)).to(q.device, non_blocking=False)
+        thr_positions = sl.shape[1]
+        mode = _lib.GATE_THRESHOLD
+    elif gate is not None:
+        mode = kernel_gate_mode(gate)
+        if mode == _lib.GATE_THRESHOLD:  # pragma: no cover - handled above
+            raise ConfigurationError("threshold gate without thresholds")
+    else:
+        mode = _lib.GATE_DENSE
+
+    n_pad = tiles.padded_len(n)
+    d_pad = 64 if d <= 64 else 128
+    sc = reference_scale(d) if scale is None else float(np.float32(scale))
+
+    dev = q.device
+    with torch.cuda.device(dev):
+        qk = _as_kernel_operand(q, n_pad, d_pad)
+        kk = _as_kernel_operand(k, n_pad, d_pad)
+        vk = _as_kernel_operand(v, n_pad, d_pad)
+        o = torch.empty((bsz, hq, n_pad, d_pad), dtype=torch.bfloat16, device=dev)
+        lse = torch.empty((bsz, hq, n_pad), dtype=torch.float32, device=dev)
+        m_q, m_kv = n_pad // tiles.b_m, n_pad // tiles.b_n
+        dec = torch.zeros((bsz, hq, m_q, m_kv), dtype=torch.int8, device=dev) if return_trace else None
+        counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        a = _lib.FwdArgs()
+        a.q, a.k, a.v = qk.data_ptr(), kk.data_ptr(), vk.data_ptr()
+        a.q_stride_b, a.q_stride_h, a.q_stride_n = qk.stride(0), qk.stride(1), qk.stride(2)
+        a.k_stride_b, a.k_stride_h, a.k_stride_n = kk.stride(0), kk.stride(1), kk.stride(2)
+        a.v_stride_b, a.v_stride_h, a.v_stride_n = vk.stride(0), vk.stride(1), vk.stride(2)
+        a.o = o.data_ptr()
+        a.o_stride_b, a.o_stride_h, a.o_stride_n = o.stride(0), o.stride(1), o.stride(2)
+        a.lse = lse.data_ptr()
+        a.decisions = dec.data_ptr() if dec is not None else None
+        a.counters = counters.data_ptr()
+        a.status = status.data_ptr()
+        a.thresholds = thr_dev.data_ptr() if thr_dev is not None else None
+        a.thr_positions = thr_positions
+        a.gate_mode = mode
+        a.batch, a.heads_q, a.heads_kv = bsz, hq, hkv
+        a.seq_len, a.valid_len, a.head_dim = n_pad, n, d_pad
+        a.b_m, a.b_n = tiles.b_m, tiles.b_n
+        a.causal = 1 if causal else 0
+        a.scale = sc
+        a.inject_fault = 1 if inject_fault else 0
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.load_library().bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
+
+    if n_pad != n or d_pad != d:
+        o = o[:, :, :n, :d]
+        lse = lse[:, :, :n]
+    if check_numerics and int(status.item()) != 0:
+        raise NumericError("non-finite accumulator or zero normaliser in at least one query row")
+    return AttentionResult(o=o, lse=lse, decisions=dec, counters=counters, status=status)
+
+
+def flash_forward(inp, tiles: TileConfig, gate, ctx: GateContext | None = None, threads: int = 1,
+                  inject_fault: bool = False, device=None) -> tuple[AttentionOutput, GateTrace]:
+    """Reference-signature single-head forward (engine.py:117-124) on the GPU.
+
+    ``threads`` is accepted for signature compatibility and ignored (the
+    kernel parallelises over query blocks by construction, bitwise
+    deterministically).  ``inp`` is a HeadInput (this package's or any object
+    with q/k/v/causal); values are rounded to bf16 on upload.
+    """
+    if ctx is None:
+        ctx = GateContext()
+    gate.validate(tiles, ctx)
+    mode = kernel_gate_mode(gate)
+    require_kernel_tiles(tiles)
+    if not isinstance(inp, HeadInput):
+        inp = HeadInput(inp.q, inp.k, inp.v, causal=bool(inp.causal))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def up(m):
+        return torch.from_numpy(m).to(dev).to(torch.bfloat16)[None, None]
+
+    kw = {}
+    if mode == _lib.GATE_THRESHOLD:
+        kw = dict(thresholds=gate.tensor, layer=ctx.layer, k_level=ctx.k_level, head_offset=ctx.head)
+    else:
+        kw = dict(gate=gate)
+    res = attention(up(inp.q), up(inp.k), up(inp.v), causal=inp.causal, tiles=tiles,
+                    return_trace=True, inject_fault=inject_fault, **kw)
+    if int(res.status.item()) != 0:
+        raise NumericError("non-finite accumulator in at least one query block")
+    o = res.o[0, 0].float().cpu().numpy()
+    lse = res.lse[0, 0].cpu().numpy()
+    trace = GateTrace(decisions=res.decisions[0, 0].cpu().numpy(), tiles=tiles,
+                      causal=inp.causal, layer=ctx.layer, head=ctx.head)
+    return AttentionOutput(o=o, logsumexp=lse), trace

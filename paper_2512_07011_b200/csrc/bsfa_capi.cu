@@ -1,0 +1,288 @@
+// C ABI (include/bsfa_b200.h): argument checking, TMA descriptor encoding and
+// kernel dispatch.  No torch types cross this boundary.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/bsfa_b200.h"
+#include "bsfa_kernel.cuh"
+
+using namespace bsfa;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(BSFA_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library does not link libcuda directly.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// 4-D bf16 view (head_dim, seq, heads, batch) with a {64, rows, 1, 1} box and
+// 128-byte swizzle -- the canonical K-major SW128 UMMA operand layout.
+int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int64_t sn, int64_t sh, int64_t sb,
+             int box_rows, const char* name) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(BSFA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the CUDA driver");
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return fail(BSFA_ERR_INVALID, "%s: base not 16-byte aligned", name);
+  if ((sn * 2) % 16 || (sh * 2) % 16 || (sb * 2) % 16)
+    return fail(BSFA_ERR_INVALID, "%s: strides must be multiples of 8 elements", name);
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)h, (cuuint64_t)bsz};
+  // dims of size 1 still need a valid stride
+  cuuint64_t strides[3] = {(cuuint64_t)(sn * 2), (cuuint64_t)((h > 1 ? sh : (int64_t)n * sn) * 2),
+                           (cuuint64_t)((bsz > 1 ? sb : (int64_t)h * (h > 1 ? sh : (int64_t)n * sn)) * 2)};
+  cuuint32_t box[4] = {64u, (cuuint32_t)box_rows, 1u, 1u};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BSFA_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed (CUresult %d)", name, (int)r);
+  return BSFA_OK;
+}
+
+template <int D, int NH, int NQ, bool CALIB>
+int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+           cudaStream_t st) {
+  using C = KCfg<D, NH, NQ, CALIB>;
+  auto kern = bsfa_kernel<D, NH, NQ, CALIB>;
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  if (grid == 0) return BSFA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
+  return BSFA_OK;
+}
+
+template <bool CALIB>
+int dispatch(int d, int nh, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+             const KernelParams& p, int grid, cudaStream_t st) {
+#define BSFA_CASE(D_, NH_, NQ_) \
+  if (d == D_ && nh == NH_ && nq == NQ_) return launch<D_, NH_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
+  BSFA_CASE(64, 1, 1)
+  BSFA_CASE(64, 1, 2)
+  BSFA_CASE(64, 2, 1)
+  BSFA_CASE(64, 2, 2)
+  BSFA_CASE(128, 1, 1)
+  BSFA_CASE(128, 1, 2)
+  BSFA_CASE(128, 2, 1)
+  BSFA_CASE(128, 2, 2)
+#undef BSFA_CASE
+  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d gate tiles/MMA tile=%d q tiles/CTA=%d", d, nh, nq);
+}
+
+int check_tiles(int b_m, int b_n) {
+  if (b_m != 128 || (b_n != 64 && b_n != 128))
+    return fail(BSFA_ERR_INVALID, "unsupported tiles %dx%d: the sm_100a kernel implements b_m=128, b_n in {64,128}",
+                b_m, b_n);
+  return BSFA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsfa_abi_version(void) { return BSFA_ABI_VERSION; }
+
+const char* bsfa_last_error(void) { return g_last_error.c_str(); }
+
+int bsfa_device_supported(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+  return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+}
+
+int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
+  if (!a) return fail(BSFA_ERR_INVALID, "null args");
+  if (int rc = check_tiles(a->b_m, a->b_n)) return rc;
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64 or 128; pad smaller heads)", a->head_dim);
+  if (a->batch < 1 || a->heads_q < 1 || a->heads_kv < 1 || a->heads_q % a->heads_kv)
+    return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d batch=%d", a->heads_q, a->heads_kv, a->batch);
+  if (a->seq_len < 128 || a->seq_len % 128)
+    return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
+  if (a->valid_len < 1 || a->valid_len > a->seq_len) return fail(BSFA_ERR_INVALID, "bad valid_len %d", a->valid_len);
+  if (a->gate_mode < 0 || a->gate_mode > 2) return fail(BSFA_ERR_INVALID, "bad gate_mode %d", a->gate_mode);
+  if (a->gate_mode == BSFA_GATE_THRESHOLD && (!a->thresholds || a->thr_positions < 1))
+    return fail(BSFA_ERR_INVALID, "threshold gate needs a [heads_q][positions] threshold array");
+  if (!a->q || !a->k || !a->v || !a->o || !a->lse) return fail(BSFA_ERR_INVALID, "null tensor pointer");
+  if (reinterpret_cast<uintptr_t>(a->o) % 16 || (a->o_stride_n * 2) % 16)
+    return fail(BSFA_ERR_INVALID, "o must be 16-byte aligned per row");
+
+  const int d = a->head_dim, n = a->seq_len;
+  CUtensorMap tq, tk, tv;
+  if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
+    return rc;
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, 128, "k"))
+    return rc;
+  if (int rc =
+          make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))
+    return rc;
+
+  KernelParams p;
+  memset(&p, 0, sizeof(p));
+  p.batch = a->batch;
+  p.heads_q = a->heads_q;
+  p.heads_kv = a->heads_kv;
+  p.group = a->heads_q / a->heads_kv;
+  p.seq_len = n;
+  p.valid_len = a->valid_len;
+  p.num_q_tiles = n / 128;
+  p.num_kv_tiles = n / 128;
+  p.gate_cols = n / a->b_n;
+  p.causal = a->causal ? 1 : 0;
+  p.gate_mode = a->gate_mode;
+  p.thr_positions = a->thr_positions;
+  p.scale = a->scale;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.rescale_raw = 8.0f / p.scale_log2;
+  p.inject_fault = a->inject_fault;
+  p.thr = a->thresholds;
+  p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
+  p.o_sb = a->o_stride_b;
+  p.o_sh = a->o_stride_h;
+  p.o_sn = a->o_stride_n;
+  p.lse = a->lse;
+  p.decisions = a->decisions;
+  p.counters = a->counters;
+  p.status = a->status;
+
+  const int nq = (p.group % 2 == 0) ? 2 : 1;
+  const int nh = 128 / a->b_n;
+  const long long grid = (long long)a->batch * a->heads_kv * (p.group / nq) * p.num_q_tiles;
+  if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
+  return dispatch<false>(d, nh, nq, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
+  if (!a) return fail(BSFA_ERR_INVALID, "null args");
+  if (int rc = check_tiles(a->b_m, a->b_n)) return rc;
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64 or 128; pad smaller heads)", a->head_dim);
+  if (a->heads_q < 1 || a->heads_kv < 1 || a->heads_q % a->heads_kv)
+    return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
+  if (a->seq_len < 128 || a->seq_len % 128)
+    return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
+  if (a->seq_len / a->b_n > KCfg<64, 2, 1, true>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, 1, true>::MAXA);
+  if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
+  if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
+  if (a->seq_len / a->b_m > a->num_positions)
+    return fail(BSFA_ERR_INVALID, "sample has %d positions > accumulator %d", a->seq_len / a->b_m, a->num_positions);
+  if (!a->q || !a->k || !a->finite_sum || !a->finite_cnt || !a->neg_cnt || !a->pos_cnt || !a->tie_counts)
+    return fail(BSFA_ERR_INVALID, "null pointer");
+
+  const int d = a->head_dim, n = a->seq_len;
+  CUtensorMap tq, tk;
+  if (int rc = make_map(&tq, a->q, d, n, a->heads_q, 1, a->q_stride_n, a->q_stride_h, 0, 128, "q")) return rc;
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, 128, "k")) return rc;
+
+  KernelParams p;
+  memset(&p, 0, sizeof(p));
+  p.batch = 1;
+  p.heads_q = a->heads_q;
+  p.heads_kv = a->heads_kv;
+  p.group = a->heads_q / a->heads_kv;
+  p.seq_len = n;
+  p.valid_len = n;
+  p.num_q_tiles = n / 128;
+  p.num_kv_tiles = n / 128;
+  p.gate_cols = n / a->b_n;
+  p.causal = 1;
+  p.scale = a->scale;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.c_layer = a->layer;
+  p.c_num_layers = a->num_layers;
+  p.c_positions = a->num_positions;
+  p.c_num_levels = a->num_levels;
+  for (int i = 0; i < a->num_levels; ++i) {
+    if (a->k_levels[i] < 0) return fail(BSFA_ERR_INVALID, "k levels must be >= 0");
+    p.c_levels[i] = a->k_levels[i];
+  }
+  p.c_sum = a->finite_sum;
+  p.c_fin = a->finite_cnt;
+  p.c_neg = a->neg_cnt;
+  p.c_pos = a->pos_cnt;
+  p.c_ties = a->tie_counts;
+  p.c_maxima = a->block_maxima;
+
+  const int nq = (p.group % 2 == 0) ? 2 : 1;
+  const int nh = 128 / a->b_n;
+  const int grid = a->heads_kv * (p.group / nq) * p.num_q_tiles;
+  return dispatch<true>(d, nh, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- finalize (K4)
+namespace {
+__global__ void calib_finalize_kernel(const double* __restrict__ sum, const int32_t* __restrict__ fin,
+                                      const int32_t* __restrict__ neg, const int32_t* __restrict__ pos,
+                                      float* __restrict__ out, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v;
+    if (fin[i] > 0)
+      v = (float)(sum[i] / (double)fin[i]);
+    else if (neg[i] > 0)
+      v = -INFINITY;
+    else if (pos[i] > 0)
+      v = INFINITY;
+    else
+      v = 0.f;
+    out[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" int bsfa_calib_finalize(const double* finite_sum, const int32_t* finite_cnt, const int32_t* neg_cnt,
+                                   const int32_t* pos_cnt, float* values, int64_t count, void* stream) {
+  if (count < 0 || (count > 0 && (!finite_sum || !finite_cnt || !neg_cnt || !pos_cnt || !values)))
+    return fail(BSFA_ERR_INVALID, "bad finalize arguments");
+  if (count == 0) return BSFA_OK;
+  const int threads = 256;
+  long long blocks = (count + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  calib_finalize_kernel<<<(int)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      finite_sum, finite_cnt, neg_cnt, pos_cnt, values, count);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
+  return BSFA_OK;
+}

@@ -1,0 +1,419 @@
+"""GPU parity: the sm_100a kernels against the CPU oracle on identical inputs.
+
+Tolerances:
+  * decisions: identical to the oracle's ThresholdGate except gated tiles whose
+    oracle block max lies within EPS of the threshold;
+  * outputs: max |O_gpu - O_ref| <= ATOL where O_ref is the oracle's fp32
+    engine replaying the GPU's decisions (same mask, bf16-valued inputs);
+  * dense (T = -inf / DenseGate): same ATOL against the fp64 dense oracle.
+"""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN, load_golden  # noqa: E402
+from oracle import bsfa_oracle as orc  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-3
+ATOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def bsfa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_07011_b200 as m
+    return m
+
+
+def _dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(torch.bfloat16 if dtype is None else dtype)
+
+
+def _mask_parity(dec_gpu, dec_ref, smax_ref, thr_of_block):
+    bad = []
+    for (i, j) in zip(*np.nonzero(dec_gpu != dec_ref)):
+        s = smax_ref[i, j]
+        if not (np.isfinite(s) and abs(s - thr_of_block(i)) <= EPS):
+            bad.append((int(i), int(j), float(s), int(dec_gpu[i, j]), int(dec_ref[i, j])))
+    return bad
+
+
+def _smax_grid(record, shape):
+    g = np.full(shape, np.nan)
+    for (i, j), v in record.items():
+        g[i, j] = v
+    return g
+
+
+# ------------------------------------------------------------------ probes first
+def test_blockmax_matches_oracle(bsfa):
+    rng = np.random.default_rng(1)
+    for d in (64, 128):
+        n = 1024
+        q = orc.round_bf16(rng.standard_normal((2, n, d)).astype(np.float32))
+        k = orc.round_bf16(rng.standard_normal((1, n, d)).astype(np.float32))
+        tiles = bsfa.TileConfig(128, 64)
+        cal = bsfa.Calibrator([0, 2], tiles, 1, 2, n, d)
+        bm = torch.full((2, n // 128, n // 64), float("nan"), device="cuda")
+        cal.add_layer(0, 0, _dev(q, torch.float32), _dev(k, torch.float32), block_maxima=bm)
+        bm = bm.cpu().numpy()
+        for h in range(2):
+            prof = orc.block_maxima(q[h], k[0], 128, 64)
+            for p, vals in enumerate(prof):
+                got = np.sort(bm[h, p, :len(vals)])[::-1]
+                np.testing.assert_allclose(got, vals, rtol=0, atol=1e-4)
+
+
+def test_dense_single_tile_vs_fp64(bsfa):
+    rng = np.random.default_rng(2)
+    for d in (64, 128):
+        q, k, v = (orc.round_bf16(rng.standard_normal((128, d)).astype(np.float32)) for _ in range(3))
+        res = bsfa.attention(_dev(q)[None, None], _dev(k)[None, None], _dev(v)[None, None], causal=True)
+        o64, lse64 = orc.dense_attention(q, k, v, True)
+        o = res.o[0, 0].float().cpu().numpy()
+        assert np.abs(o - o64).max() <= ATOL, f"d={d}"
+        np.testing.assert_allclose(res.lse[0, 0].cpu().numpy(), lse64, atol=1e-2)
+
+
+@pytest.mark.parametrize("n,d,causal", [(256, 64, True), (1024, 64, True), (1024, 128, True),
+                                        (512, 128, False), (130, 64, True), (257, 128, False),
+                                        (2048, 128, True)])
+def test_dense_vs_fp64(bsfa, n, d, causal):
+    rng = np.random.default_rng(n + d)
+    q, k, v = (orc.round_bf16(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3))
+    res = bsfa.attention(_dev(q)[None, None], _dev(k)[None, None], _dev(v)[None, None], causal=causal,
+                         return_trace=True)
+    o64, lse64 = orc.dense_attention(q, k, v, causal)
+    o = res.o[0, 0].float().cpu().numpy()
+    assert np.abs(o - o64).max() <= ATOL
+    np.testing.assert_allclose(res.lse[0, 0].cpu().numpy(), lse64, atol=1e-2)
+    dec = res.decisions[0, 0].cpu().numpy()
+    _, _, dec_ref = orc.flash_forward(q, k, v, causal, 128, 64, orc.dense_gate)
+    np.testing.assert_array_equal(dec, dec_ref)
+
+
+# ------------------------------------------------------------------ golden engine cases
+GOLDEN_ENGINE = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "engine_*.npz")))
+
+
+@pytest.mark.parametrize("name", GOLDEN_ENGINE)
+def test_golden_engine_case(bsfa, name):
+    c = load_golden(name)
+    b_m, b_n, causal, kind = int(c["b_m"]), int(c["b_n"]), bool(c["causal"]), str(c["kind"])
+    tiles = bsfa.TileConfig(b_m, b_n)
+    if not bsfa.kernel_supports(tiles):
+        with pytest.raises(bsfa.ConfigurationError):
+            bsfa.flash_forward(bsfa.HeadInput(c["q"], c["k"], c["v"], causal=causal), tiles, bsfa.dense_gate())
+        return
+    n = c["q"].shape[0]
+    if kind == "dense":
+        gate, ctx = bsfa.dense_gate(), bsfa.GateContext()
+    elif kind == "frontier":
+        gate, ctx = bsfa.frontier_only_gate(), bsfa.GateContext()
+    else:
+        t = bsfa.ThresholdTensor(values=c["thr"][None, None, None], k_levels=(4,),
+                                 n_max=tiles.padded_len(n), b_m=b_m, b_n=b_n)
+        gate, ctx = bsfa.threshold_gate(t), bsfa.GateContext(k_level=4)
+    out, trace = bsfa.flash_forward(bsfa.HeadInput(c["q"], c["k"], c["v"], causal=causal), tiles, gate, ctx)
+    assert out.o.shape == c["o"].shape
+    if kind == "threshold":
+        thr = c["thr"]
+        bad = _mask_parity(trace.decisions, c["decisions"], c["smax"], lambda i: thr[min(i, len(thr) - 1)])
+        assert not bad, bad[:5]
+    else:
+        np.testing.assert_array_equal(trace.decisions, c["decisions"])
+    o_ref, lse_ref, _ = orc.flash_forward(c["q"], c["k"], c["v"], causal, b_m, b_n,
+                                          orc.replay_gate(trace.decisions))
+    assert np.abs(out.o - o_ref).max() <= ATOL
+    np.testing.assert_allclose(out.logsumexp, lse_ref, atol=1e-2)
+
+
+def test_toy_config(bsfa):
+    c = load_golden("toy")
+    tiles = bsfa.TileConfig(128, 64)
+    inp = bsfa.HeadInput(c["q"], c["k"], c["v"])
+    for key, gate, ctx in (("dense", bsfa.dense_gate(), bsfa.GateContext()),
+                           ("frontier", bsfa.frontier_only_gate(), bsfa.GateContext())):
+        out, trace = bsfa.flash_forward(inp, tiles, gate, ctx)
+        np.testing.assert_array_equal(trace.decisions, c[f"dec_{key}"])
+        assert np.abs(out.o - c[f"o_{key}"]).max() <= ATOL
+    T = float(c["T"])
+    for t_val, expect in ((-np.inf, "dense"), (np.inf, "frontier"), (T, None)):
+        t = bsfa.ThresholdTensor(values=np.full((1, 1, 1, 8), t_val, dtype=np.float32), k_levels=(1,),
+                                 n_max=1024, b_m=128, b_n=64)
+        out, trace = bsfa.flash_forward(inp, tiles, bsfa.threshold_gate(t), bsfa.GateContext(k_level=1))
+        if expect is not None:
+            np.testing.assert_array_equal(trace.decisions, c[f"dec_{expect}"])
+            assert np.abs(out.o - c[f"o_{expect}"]).max() <= ATOL
+        else:
+            bad = _mask_parity(trace.decisions, c["dec_thr"], c["smax"], lambda i: T)
+            assert not bad, bad[:5]
+            o_ref, _, _ = orc.flash_forward(c["q"], c["k"], c["v"], True, 128, 64, orc.replay_gate(trace.decisions))
+            assert np.abs(out.o - o_ref).max() <= ATOL
+
+
+# ------------------------------------------------------------------ batched / GQA
+@pytest.mark.parametrize("b_n", [64, 128])
+@pytest.mark.parametrize("hq,hkv,d", [(8, 2, 128), (4, 4, 64), (6, 2, 64), (3, 1, 128)])
+def test_gqa_batched_threshold(bsfa, b_n, hq, hkv, d):
+    rng = np.random.default_rng(hq * 31 + hkv + d + b_n)
+    B, n = 2, 1024
+    q = orc.round_bf16(rng.standard_normal((B, hq, n, d)).astype(np.float32))
+    k = orc.round_bf16(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    v = orc.round_bf16(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    tiles = bsfa.TileConfig(128, b_n)
+    P = n // 128
+    base = 3.6 if d == 128 else 3.3
+    vals = (base + 0.3 * rng.standard_normal((2, 3, hq, P))).astype(np.float32)
+    vals = np.sort(vals, axis=0)[::-1].copy()  # monotone in k
+    t = bsfa.ThresholdTensor(values=vals, k_levels=(2, 5), n_max=n, b_m=128, b_n=b_n)
+    res = bsfa.attention(_dev(q), _dev(k), _dev(v), thresholds=t, layer=1, k_level=5, tiles=tiles,
+                         return_trace=True)
+    o = res.o.float().cpu().numpy()
+    dec = res.decisions.cpu().numpy()
+    cnt = res.counters.cpu().numpy()
+    assert cnt[0] == np.count_nonzero(dec != 0)
+    assert cnt[1] == np.count_nonzero(dec >= 2)
+    g = hq // hkv
+    for b in range(B):
+        for h in range(hq):
+            thr_h = vals[1, 1, h]
+            rec = {}
+            _, _, dec_ref = orc.flash_forward(q[b, h], k[b, h // g], v[b, h // g], True, 128, b_n,
+                                              orc.threshold_gate(thr_h), record=rec)
+            bad = _mask_parity(dec[b, h], dec_ref, _smax_grid(rec, dec_ref.shape),
+                               lambda i: thr_h[min(i, P - 1)])
+            assert not bad, (b, h, bad[:5])
+            o_ref, _, _ = orc.flash_forward_fast(q[b, h], k[b, h // g], v[b, h // g], True, 128, b_n,
+                                                 lambda i_idx, j, sm: dec[b, h][i_idx, j] == orc.KEPT)
+            assert np.abs(o[b, h] - o_ref).max() <= ATOL, (b, h)
+
+
+def test_noncausal_padding_threshold(bsfa):
+    rng = np.random.default_rng(11)
+    n, d = 300, 64
+    q, k, v = (orc.round_bf16(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3))
+    tiles = bsfa.TileConfig(128, 64)
+    thr = np.float32(0.9)
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, 1, 3), thr, dtype=np.float32), k_levels=(1,),
+                             n_max=384, b_m=128, b_n=64)
+    out, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v, causal=False), tiles, bsfa.threshold_gate(t),
+                                    bsfa.GateContext(k_level=1))
+    rec = {}
+    o_thr, _, dec_ref = orc.flash_forward(q, k, v, False, 128, 64, orc.threshold_gate([thr]), record=rec)
+    bad = _mask_parity(trace.decisions, dec_ref, _smax_grid(rec, dec_ref.shape), lambda i: thr)
+    assert not bad
+    o_ref, _, _ = orc.flash_forward(q, k, v, False, 128, 64, orc.replay_gate(trace.decisions))
+    assert np.abs(out.o - o_ref).max() <= ATOL
+
+
+# ------------------------------------------------------------------ semantics / plumbing
+def test_small_head_dim_zero_padding_kats(bsfa):
+    # reference tests/test_core.py:10-22 through the GPU drop-in (d=1, d=2 padded to 64)
+    tiles = bsfa.TileConfig(128, 64)
+    out, _ = bsfa.flash_forward(bsfa.HeadInput(q=[[1.0], [1.0]], k=[[0.0], [0.0]], v=[[1.0], [4.2]]),
+                                tiles, bsfa.dense_gate())
+    np.testing.assert_allclose(out.o, [[1.0], [2.6]], atol=2e-2)
+    np.testing.assert_allclose(out.logsumexp, [0.0, np.log(2.0)], atol=1e-3)
+    out, _ = bsfa.flash_forward(bsfa.HeadInput(q=[[1.0, 2.0]], k=[[3.0, 4.0]], v=[[3.0, 7.0]]), tiles,
+                                bsfa.dense_gate())
+    np.testing.assert_allclose(out.o, [[3.0, 7.0]], atol=2e-2)
+    np.testing.assert_allclose(out.logsumexp, [11.0 / np.sqrt(2.0)], atol=1e-3)
+
+
+def test_trace_decision_codes(bsfa):
+    # reference tests/test_engine.py:50-67
+    rng = np.random.default_rng(8)
+    q, k, v = (rng.standard_normal((256, 16)) for _ in range(3))
+    tiles = bsfa.TileConfig(128, 64)
+    _, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.dense_gate())
+    np.testing.assert_array_equal(trace.decisions, [[2, 2, 0, 0], [3, 3, 2, 2]])
+    assert trace.kept_blocks() == 6 and trace.reachable_blocks() == 6 and trace.density() == 1.0
+    np.testing.assert_array_equal(trace.retained_off_frontier(), [0, 2])
+    _, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.frontier_only_gate())
+    assert trace.decisions[1, 0] == 1 and trace.density() == pytest.approx(4 / 6)
+
+
+def test_strict_threshold_equality_skips(bsfa):
+    # keep iff s_max > T: a tile whose max equals T exactly is skipped (gates.py:78, test_gates.py:23-27)
+    d, n = 64, 256
+    q = np.zeros((n, d), dtype=np.float32)
+    k = np.zeros((n, d), dtype=np.float32)
+    q[:, 0] = 1.0
+    k[:, 0] = 2.0  # every score = 2 * scale exactly (power-of-two arithmetic)
+    v = np.ones((n, d), dtype=np.float32)
+    tiles = bsfa.TileConfig(128, 64)
+    s = np.float32(2.0) * np.float32(1.0 / np.sqrt(d))
+    for T, code in ((s, 1), (np.nextafter(s, np.float32(0)), 3)):
+        t = bsfa.ThresholdTensor(values=np.full((1, 1, 1, 2), T, dtype=np.float32), k_levels=(1,),
+                                 n_max=n, b_m=128, b_n=64)
+        _, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.threshold_gate(t),
+                                      bsfa.GateContext(k_level=1))
+        assert trace.decisions[1, 0] == code and trace.decisions[1, 1] == code
+
+
+def test_threshold_position_clamp(bsfa):
+    # query blocks beyond the calibrated range reuse position P-1 (thresholds.py:87)
+    rng = np.random.default_rng(3)
+    n, d = 1024, 64
+    q, k, v = (orc.round_bf16(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3))
+    vals = np.array([[[[np.inf, -np.inf]]]], dtype=np.float32)  # P=2: block 0 skip-all, blocks >=1 keep-all
+    t = bsfa.ThresholdTensor(values=vals, k_levels=(1,), n_max=256, b_m=128, b_n=64)
+    _, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), bsfa.TileConfig(128, 64), bsfa.threshold_gate(t),
+                                  bsfa.GateContext(k_level=1))
+    dec = trace.decisions
+    for i in range(1, 8):
+        assert (dec[i, :2 * i] == 3).all()
+
+
+def test_determinism_and_counters(bsfa):
+    rng = np.random.default_rng(4)
+    B, hq, hkv, n, d = 1, 4, 2, 2048, 128
+    q = _dev(rng.standard_normal((B, hq, n, d)).astype(np.float32))
+    k = _dev(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    v = _dev(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, hq, 16), 3.7, dtype=np.float32), k_levels=(3,),
+                             n_max=n, b_m=128, b_n=64)
+    r1 = bsfa.attention(q, k, v, thresholds=t, k_level=3, return_trace=True)
+    r2 = bsfa.attention(q, k, v, thresholds=t, k_level=3, return_trace=True)
+    assert torch.equal(r1.o, r2.o) and torch.equal(r1.lse, r2.lse) and torch.equal(r1.decisions, r2.decisions)
+    dec = r1.decisions.cpu().numpy()
+    c = r1.counters.cpu().numpy()
+    assert c[0] == np.count_nonzero(dec) and c[1] == np.count_nonzero(dec >= 2)
+    # V tiles fetched = union over the two q heads sharing a kv head of kept/frontier tiles
+    vload = sum(np.count_nonzero((dec[0, 2 * g] >= 2) | (dec[0, 2 * g + 1] >= 2)) for g in range(hkv))
+    assert c[2] == vload
+    assert 0 < c[1] < c[0]
+
+
+def test_inject_fault_is_detected(bsfa):
+    rng = np.random.default_rng(10)
+    q, k, v = (rng.standard_normal((128, 64)) for _ in range(3))
+    tiles = bsfa.TileConfig(128, 64)
+    clean, _ = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.dense_gate())
+    dirty, _ = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.dense_gate(), inject_fault=True)
+    assert not np.array_equal(clean.o, dirty.o)
+    o64, _ = orc.dense_attention(orc.round_bf16(np.asarray(q, np.float32)), orc.round_bf16(np.asarray(k, np.float32)),
+                                 orc.round_bf16(np.asarray(v, np.float32)))
+    assert np.abs(dirty.o - o64).max() > ATOL
+
+
+def test_unsupported_gate_and_tiles_refused(bsfa):
+    rng = np.random.default_rng(0)
+    inp = bsfa.HeadInput(*(rng.standard_normal((128, 64)) for _ in range(3)))
+
+    class Sliding:
+        def validate(self, tiles, ctx):
+            pass
+
+        def decide(self, *a):
+            return True
+
+    with pytest.raises(bsfa.ConfigurationError):
+        bsfa.flash_forward(inp, bsfa.TileConfig(128, 64), Sliding())
+    with pytest.raises(bsfa.ConfigurationError):
+        bsfa.flash_forward(inp, bsfa.TileConfig(64, 64), bsfa.dense_gate())
+
+
+# ------------------------------------------------------------------ calibration
+def test_calibration_matches_reference_golden(bsfa):
+    c = load_golden("calib")
+    samples = [bsfa.CalibrationSample(sample_id=i, q=c[f"q{i}"], k=c[f"k{i}"]) for i in (1, 2, 0)]
+    t = bsfa.calibrate(bsfa.CalibrationDump(1, 2, 64, samples), [int(x) for x in c["k_levels"]],
+                       bsfa.TileConfig(128, 64))
+    ref = c["values"]
+    assert t.n_max == int(c["n_max"]) and t.values.shape == ref.shape
+    fin = np.isfinite(ref)
+    np.testing.assert_array_equal(np.isfinite(t.values), fin)
+    np.testing.assert_array_equal(t.values[~fin], ref[~fin])
+    assert np.abs(t.values[fin] - ref[fin]).max() <= 1e-4
+    prof = bsfa.collect_block_maxima(samples[0], bsfa.TileConfig(128, 64))  # sample id 1
+    for p in range(8):
+        vals = prof.maxima[(0, 1, p)]
+        np.testing.assert_allclose(vals, c["maxima_sample1"][0, 1, p, :len(vals)], atol=1e-4)
+
+
+def test_topk_round_trip_on_gpu(bsfa):
+    # reference acceptance 3 (test_acceptance.py:94-117): calibrate on a sample, run the gate on
+    # the same sample -> every position retains exactly min(k, A_p) off-frontier tiles.
+    rng = np.random.default_rng(12)
+    L, H, Hkv, n, d = 2, 4, 2, 2048, 128
+    q = orc.round_bf16(rng.standard_normal((L, H, n, d)).astype(np.float32))
+    k = orc.round_bf16(rng.standard_normal((L, Hkv, n, d)).astype(np.float32))
+    v = orc.round_bf16(rng.standard_normal((L, Hkv, n, d)).astype(np.float32))
+    tiles = bsfa.TileConfig(128, 64)
+    k_levels = [1, 4, 9, 16]
+    t = bsfa.calibrate(bsfa.CalibrationDump(L, H, d, [bsfa.CalibrationSample(0, q, k)]), k_levels, tiles)
+    assert all(x == 0 for x in t.diagnostics.tie_counts.values())
+    mism = 0
+    for kk in k_levels:
+        for layer in range(L):
+            res = bsfa.attention(_dev(q[layer])[None], _dev(k[layer])[None], _dev(v[layer])[None],
+                                 thresholds=t, layer=layer, k_level=kk, return_trace=True)
+            dec = res.decisions[0].cpu().numpy()
+            for h in range(H):
+                kept = np.count_nonzero(dec[h] == 3, axis=1)
+                target = np.minimum(kk, 2 * np.arange(n // 128))
+                mism += int(np.count_nonzero(kept != target))
+    assert mism == 0
+
+
+def test_threshold_file_round_trip_gpu_tensor(bsfa, tmp_path):
+    c = load_golden("calib")
+    samples = [bsfa.CalibrationSample(sample_id=i, q=c[f"q{i}"], k=c[f"k{i}"]) for i in (0, 1, 2)]
+    t = bsfa.calibrate(bsfa.CalibrationDump(1, 2, 64, samples), [0, 1, 3, 6, 99], bsfa.TileConfig(128, 64))
+    bsfa.save_thresholds(t, tmp_path / "t.bin")
+    u = bsfa.load_thresholds(tmp_path / "t.bin")
+    np.testing.assert_array_equal(u.values, t.values)
+    bsfa.save_thresholds(u, tmp_path / "u.bin")
+    assert (tmp_path / "t.bin").read_bytes() == (tmp_path / "u.bin").read_bytes()
+    ref_bytes = c["file_bytes"].tobytes()
+    assert len(ref_bytes) == len((tmp_path / "t.bin").read_bytes())
+    assert ref_bytes[:36] == (tmp_path / "t.bin").read_bytes()[:36]  # identical header
+
+
+# ------------------------------------------------------------------ full size (sampled heads)
+@pytest.mark.parametrize("n", [32768])
+def test_llama_shape_sampled_heads(bsfa, n):
+    """L32K Llama-3.1-8B shape (32 q / 8 kv heads, d=128): dense and ~50% skip, two heads checked."""
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn((1, 32, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, 8, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, 8, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    T = 3.84
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, 32, n // 128), T, dtype=np.float32), k_levels=(1,),
+                             n_max=n, b_m=128, b_n=64)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True)
+    dense = bsfa.attention(q, k, v, return_trace=False)
+    cnt = res.counters.cpu().numpy()
+    skip = 1 - (cnt[1] - 0) / cnt[0]
+    assert 0.2 < skip < 0.7
+    for h in (0, 29):
+        qh = q[0, h].float().cpu().numpy()
+        kh = k[0, h // 4].float().cpu().numpy()
+        vh = v[0, h // 4].float().cpu().numpy()
+        dec = res.decisions[0, h].cpu().numpy()
+        rec = {}
+
+        def keep_fn(i_idx, j, smax):
+            return dec[i_idx, j] == orc.KEPT
+
+        o_ref, _, dec_ref = orc.flash_forward_fast(qh, kh, vh, True, 128, 64, keep_fn, record=rec)
+        # mask parity: the GPU decision must agree with T on every tile away from the threshold
+        for j, (i_idx, smax) in rec.items():
+            far = np.abs(smax - T) > EPS
+            want = np.where(smax > T, orc.KEPT, orc.SKIPPED)
+            assert (dec[i_idx[far], j] == want[far]).all(), (h, j)
+        assert np.abs(res.o[0, h].float().cpu().numpy() - o_ref).max() <= ATOL
+        od_ref, _, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+                                              lambda i_idx, j, sm: np.ones(len(i_idx), bool))
+        assert np.abs(dense.o[0, h].float().cpu().numpy() - od_ref).max() <= ATOL
