@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the BSFA forward hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config l32k|l64k|l128k|toy] [--density 0.5]
+
+A *step* is one BSFA prefill forward over the whole workload: the
+Llama-3.1-8B attention shape (B=1 per GPU, 32 q / 8 kv heads, d=128, causal,
+bf16, 128x64 tiles) at N=32768 (BASELINE configs[1]), thresholds calibrated
+on separate synthetic data for ~50% block skip.  Inputs are synthetic
+(seeded N(0,1)); the 384 MiB of Q/K/V per step exceed the 126 MB L2, so no
+explicit flush is done between steps.
+
+Reported (one JSON line on rank 0):
+  value       executed TFLOP/s of the whole job (QK on every reachable tile,
+              PV on every kept tile; the kernel's own counters), inputs
+              resident in HBM, CUDA-event timed, max over ranks
+  e2e         the same metric through the public API from pinned host
+              buffers, H2D of Q/K/V and D2H of O inside the timed region
+  roofline    tensor-core bound; achieved = F_exec per launch / mean launch
+              time vs the measured bf16 peak (MEASURED_PEAKS.json)
+  cpu_baseline  the oracle port of the reference engine on one host core
+  dense_*     the same kernel with the DenseGate (T = -inf), for speedup
+Multi-GPU (torchrun): weak scaling, rank r owns batch element r (its own
+full 32-head workload), no data-path collective.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BSFA prefill ms & TFLOPS/GPU at 32K–128K vs dense; tensor-pipe util; skip %"
+
+CONFIGS = {
+    "toy": dict(heads_q=1, heads_kv=1, seq_len=1024, head_dim=64),
+    "l32k": dict(heads_q=32, heads_kv=8, seq_len=32768, head_dim=128),
+    "l64k": dict(heads_q=32, heads_kv=8, seq_len=65536, head_dim=128),
+    "l128k": dict(heads_q=32, heads_kv=8, seq_len=131072, head_dim=128),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="l32k")
+    ap.add_argument("--density", type=float, default=0.5, help="target kept fraction (predicted)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+def committed_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def __enter__(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.file is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.file.flush()
+        rows = []
+        with open(self.file.name) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- workload
+def make_inputs(cfg, seed, device):
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    n, d = cfg["seq_len"], cfg["head_dim"]
+    q = torch.randn((1, cfg["heads_q"], n, d), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    k = torch.randn((1, cfg["heads_kv"], n, d), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    v = torch.randn((1, cfg["heads_kv"], n, d), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    return q, k, v
+
+
+def calibrated_thresholds(cfg, tiles, k_level, device):
+    """Calibrate one layer on a separate synthetic sample (seed 1000) on the GPU."""
+    import paper_2512_07011_b200 as bsfa
+    q, k, _ = make_inputs(cfg, 1000, device)
+    cal = bsfa.Calibrator([k_level], tiles, 1, cfg["heads_q"], cfg["seq_len"], cfg["head_dim"], device=device)
+    cal.add_layer(0, 0, q[0], k[0])
+    return cal.finish()
+
+
+def time_steps(fn, steps, warmup, stream):
+    """Per-step CUDA-event times (ms) on `stream`, synchronised on both sides."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    start_all = torch.cuda.Event(enable_timing=True)
+    end_all = torch.cuda.Event(enable_timing=True)
+    start_all.record(stream)
+    for a, b in evs:
+        a.record(stream)
+        fn()
+        b.record(stream)
+    end_all.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs], start_all.elapsed_time(end_all)
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline_port(cfg, tiles, T_slice, seconds_budget=20.0):
+    """Oracle port of the reference engine (engine.py:117-193) on one host core.
+
+    Sample: head 0 of the workload, query blocks taken from the end of the
+    sequence (longest rows first) until ~`seconds_budget` of work; value is
+    executed TFLOP/s over the tiles processed.
+    """
+    import numpy as np
+    import torch
+    from threadpoolctl import threadpool_limits
+    from oracle import bsfa_oracle as orc
+    from paper_2512_07011_b200 import costs
+
+    q, k, v = make_inputs(cfg, 0, "cuda")
+    qh, kh, vh = (x[0, 0].float().cpu().numpy() for x in (q, k, v))
+    del q, k, v
+    thr = np.asarray(T_slice[0], dtype=np.float32)
+    gate = orc.threshold_gate(thr)
+    n, d = cfg["seq_len"], cfg["head_dim"]
+    m_q = n // tiles.b_m
+    done_blocks, reach, kept = 0, 0, 0
+    t0 = time.perf_counter()
+    with threadpool_limits(limits=1):
+        i = m_q - 1
+        while i >= 0 and time.perf_counter() - t0 < seconds_budget:
+            _, _, dec = orc.flash_forward(qh, kh, vh, True, tiles.b_m, tiles.b_n, gate, q_blocks=range(i, i + 1))
+            reach += int(np.count_nonzero(dec[i]))
+            kept += int(np.count_nonzero(dec[i] >= 2))
+            done_blocks += 1
+            i -= 1
+    dt = time.perf_counter() - t0
+    fl = costs.executed_flops(reach, kept, tiles, d)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
+            "sample": f"head 0, last {done_blocks} of {m_q} query blocks ({reach} tiles) of the {n}-token "
+                      f"workload, threshold gate, numpy oracle port, 1 thread, {dt:.1f} s"}
+
+
+def _ref_worker(argv):
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import bsfa_oracle as orc
+    seed, h, n, d, b_m, b_n, thr, blocks = argv
+    q, k, v = orc.gen_random(n, d, seed=seed, head=h)
+    gate = orc.threshold_gate(np.asarray(thr, np.float32))
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        _, _, dec = orc.flash_forward(q, k, v, True, b_m, b_n, gate, q_blocks=blocks)
+        dt = time.perf_counter() - t0
+    sel = dec[list(blocks)]
+    return int(np.count_nonzero(sel)), int(np.count_nonzero(sel >= 2)), dt
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm (oracle port) on all host cores."""
+    import multiprocessing as mp
+    import numpy as np
+    from paper_2512_07011_b200 import costs
+    from paper_2512_07011_b200.tiling import TileConfig
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    tiles = TileConfig(128, 64)
+    n, d = cfg["seq_len"], cfg["head_dim"]
+    m_q = n // tiles.b_m
+    cores = os.cpu_count() or 1
+    thr = [3.84] if d == 128 else [3.94]
+    # one step: every core runs one head over a bounded block of query rows near the end
+    per = max(1, min(m_q, 2))
+    jobs = [(0, h % cfg["heads_q"], n, d, tiles.b_m, tiles.b_n, thr, range(m_q - per, m_q)) for h in range(cores)]
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, jobs)
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                fl = sum(costs.executed_flops(r, kp, tiles, d) for r, kp, _ in res)
+                times.append((dt, fl))
+    tot_t = sum(t for t, _ in times)
+    tot_f = sum(f for _, f in times)
+    val = tot_f / tot_t / 1e12
+    sample = (f"{cores} processes x 1 thread, each the last {per} query blocks of one head of the "
+              f"{n}-token workload (threshold gate), numpy oracle port of engine.py")
+    line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": args.config, **cfg, "tiles": "128x64", "causal": True},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import paper_2512_07011_b200 as bsfa
+    from paper_2512_07011_b200 import costs
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    tiles = bsfa.TileConfig(128, 64)
+    n, d, hq, hkv = cfg["seq_len"], cfg["head_dim"], cfg["heads_q"], cfg["heads_kv"]
+    k_level = costs.k_for_density(n, tiles, args.density)
+    thr = calibrated_thresholds(cfg, tiles, k_level, dev)
+
+    q, k, v = make_inputs(cfg, rank, dev)  # rank r = batch element r (weak scaling)
+    plan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.run(q, k, v)
+
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        per_step, total_ms = time_steps(step, args.steps, args.warmup, stream)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = clk.summary()
+    cnt = plan.counters.cpu().numpy()
+    reach, kept, vload = int(cnt[0]), int(cnt[1]), int(cnt[2])
+    f_exec = costs.executed_flops(reach, kept, tiles, d)
+    f_dense = costs.dense_flops(reach, tiles, d)
+    ms_rank = total_ms / args.steps
+    ms = max_over_ranks(ms_rank, world)
+    job_flops = sum_over_ranks(float(f_exec), world)
+    value = job_flops / (ms * 1e-3) / 1e12
+    mean_launch_ms = sum(per_step) / len(per_step)
+
+    # dense reference point: same kernel, DenseGate
+    dense = {}
+    if not args.no_dense:
+        dplan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, device=dev)
+        dt, dtot = time_steps(lambda: dplan.run(q, k, v), max(3, args.steps // 2), 2, stream)
+        dms = max_over_ranks(dtot / max(3, args.steps // 2), world)
+        dense = {"dense_ms_per_step": dms, "speedup_vs_dense": dms / ms,
+                 "dense_tflops": sum_over_ranks(float(f_dense), world) / (dms * 1e-3) / 1e12}
+        del dplan
+
+    # end to end through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        kh = k.cpu().pin_memory()
+        vh = v.cpu().pin_memory()
+        oh = torch.empty(plan.o.shape, dtype=torch.bfloat16).pin_memory()
+        h2d = qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2
+        d2h = oh.numel() * 2
+
+        def e2e_step():
+            qd = qh.to(dev, non_blocking=True)
+            kd = kh.to(dev, non_blocking=True)
+            vd = vh.to(dev, non_blocking=True)
+            o = plan.run(qd, kd, vd)
+            oh.copy_(o, non_blocking=True)
+
+        et, etot = time_steps(e2e_step, max(3, args.steps // 2), 2, stream)
+        ems = max_over_ranks(etot / max(3, args.steps // 2), world)
+        e2e = {"value": job_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    peak, peak_sus, peak_src = measured_peaks()
+    achieved = f_exec / (mean_launch_ms * 1e-3) / 1e12
+    traffic = committed_traffic()
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus, "peak_source": peak_src,
+                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "algorithmic_flops_per_launch": f_exec}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_port(cfg, tiles, thr.layer_slice(k_level, 0))
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": args.config, "batch_per_gpu": 1, "global_batch": world, **cfg,
+                       "tiles": "128x64", "causal": True, "k_level": k_level,
+                       "predicted_density": costs.predicted_density(n, tiles, k_level),
+                       "parallelism": f"kv-group/batch sharding x{world}, no collective",
+                       "l2": "inputs (Q/K/V 384 MiB at 32K) exceed the 126 MB L2; no explicit flush",
+                       "thresholds": "calibrated on a separate synthetic sample (seed 1000)"},
+            "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / reach,
+            "effective_dense_tflops": sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12 if world == 1
+            else None,
+            **dense, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": args.steps, "per_step_ms": [round(x, 4) for x in per_step],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -142,11 +142,13 @@ def running_max_gate(lam):
 
 # ----------------------------------------------------------------- engine
 # engine.py:117-193, tile by tile
-def flash_forward(q, k, v, causal, b_m, b_n, gate, record=None):
+def flash_forward(q, k, v, causal, b_m, b_n, gate, record=None, q_blocks=None):
     """Tiled online-softmax forward with a per-off-frontier-tile gate.
 
     Returns (o, lse, decisions) with decisions on the padded grid.  If
     ``record`` is a dict, ``record[(i, j)] = s_max`` for every gated tile.
+    ``q_blocks`` restricts the run to those query blocks (query blocks are
+    independent; rows of other blocks are left uninitialised).
     """
     q = np.ascontiguousarray(q, dtype=np.float32)
     k = np.ascontiguousarray(k, dtype=np.float32)
@@ -161,7 +163,7 @@ def flash_forward(q, k, v, causal, b_m, b_n, gate, record=None):
     lse = np.empty(n, dtype=np.float32)
     dec = np.zeros((m_q, m_kv), dtype=np.int8)
     neg_inf = np.float32(-np.inf)
-    for i in range(m_q):
+    for i in (range(m_q) if q_blocks is None else q_blocks):
         fr = frontier(i, b_m, b_n)
         last = fr.stop - 1 if causal else m_kv - 1
         m = np.full(b_m, -np.inf, dtype=np.float32)

@@ -16,7 +16,7 @@ from .gates import (DenseGate, FrontierOnlyGate, GateContext, ThresholdGate, den
                     frontier_only_gate, threshold_gate)
 from .core import AttentionOutput, BlockMask, HeadInput
 from .trace import FRONTIER, KEPT, SKIPPED, UNREACHABLE, GateTrace
-from .attention import AttentionResult, attention, flash_forward, reference_scale
+from .attention import AttentionResult, BsfaPlan, attention, flash_forward, reference_scale
 from .calibration import (BlockMaximaProfile, CalibrationDiagnostics, CalibrationDump,
                           CalibrationSample, Calibrator, calibrate, collect_block_maxima)
 

@@ -226,3 +226,86 @@ def flash_forward(inp, tiles: TileConfig, gate, ctx: GateContext | None = None, 
     trace = GateTrace(decisions=res.decisions[0, 0].cpu().numpy(), tiles=tiles,
                       causal=inp.causal, layer=ctx.layer, head=ctx.head)
     return AttentionOutput(o=o, logsumexp=lse), trace
+
+
+class BsfaPlan:
+    """Pre-built launch for a fixed shape: device buffers and C-ABI arguments made once.
+
+    ``run(q, k, v)`` is then one ``bsfa_fwd`` launch (plus a counter reset)
+    on the current stream -- the form used by serving loops, CUDA graphs and
+    the benchmark.  q/k/v must already have the padded shape the plan was
+    built for ([B, Hq, n_pad, d] bf16, d in {64, 128}, row stride 16-B aligned).
+    """
+
+    def __init__(self, batch: int, heads_q: int, heads_kv: int, seq_len: int, head_dim: int, *,
+                 causal: bool = True, tiles: TileConfig = TileConfig(), thresholds: ThresholdTensor | None = None,
+                 layer: int = 0, k_level: int | None = None, head_offset: int = 0, gate=None,
+                 return_trace: bool = False, device=None):
+        require_kernel_tiles(tiles)
+        if head_dim not in (64, 128):
+            raise InvalidInputError("plans take head_dim 64 or 128 (pad smaller heads)")
+        if heads_q % heads_kv:
+            raise InvalidInputError(f"query heads {heads_q} must be a multiple of kv heads {heads_kv}")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.tiles = tiles
+        self.n = seq_len
+        self.n_pad = tiles.padded_len(seq_len)
+        self.shape_q = (batch, heads_q, self.n_pad, head_dim)
+        self.shape_kv = (batch, heads_kv, self.n_pad, head_dim)
+        dev = self.device
+        self.thr = None
+        if thresholds is None and isinstance(gate, ThresholdGate):
+            thresholds = gate.tensor
+        if thresholds is not None:
+            ThresholdGate(thresholds).validate(tiles, GateContext(layer=layer, k_level=k_level))
+            thresholds.check_site(layer, head_offset)
+            if head_offset + heads_q > thresholds.num_heads:
+                raise ConfigurationError("plan heads exceed the calibrated head range")
+            sl = thresholds.layer_slice(k_level, layer)[head_offset:head_offset + heads_q]
+            self.thr = torch.from_numpy(np.ascontiguousarray(sl)).to(dev)
+            mode = _lib.GATE_THRESHOLD
+        elif gate is not None:
+            mode = kernel_gate_mode(gate)
+        else:
+            mode = _lib.GATE_DENSE
+        self.o = torch.empty(self.shape_q, dtype=torch.bfloat16, device=dev)
+        self.lse = torch.empty((batch, heads_q, self.n_pad), dtype=torch.float32, device=dev)
+        m_q, m_kv = self.n_pad // tiles.b_m, self.n_pad // tiles.b_n
+        self.decisions = (torch.zeros((batch, heads_q, m_q, m_kv), dtype=torch.int8, device=dev)
+                          if return_trace else None)
+        self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        a = _lib.FwdArgs()
+        a.o = self.o.data_ptr()
+        a.o_stride_b, a.o_stride_h, a.o_stride_n = self.o.stride(0), self.o.stride(1), self.o.stride(2)
+        a.lse = self.lse.data_ptr()
+        a.decisions = self.decisions.data_ptr() if self.decisions is not None else None
+        a.counters = self.counters.data_ptr()
+        a.status = self.status.data_ptr()
+        a.thresholds = self.thr.data_ptr() if self.thr is not None else None
+        a.thr_positions = self.thr.shape[1] if self.thr is not None else 0
+        a.gate_mode = mode
+        a.batch, a.heads_q, a.heads_kv = batch, heads_q, heads_kv
+        a.seq_len, a.valid_len, a.head_dim = self.n_pad, seq_len, head_dim
+        a.b_m, a.b_n = tiles.b_m, tiles.b_n
+        a.causal = 1 if causal else 0
+        a.scale = reference_scale(head_dim)
+        a.inject_fault = 0
+        self.args = a
+        self.lib = _lib.load_library()
+
+    def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, reset_counters: bool = True) -> torch.Tensor:
+        if tuple(q.shape) != self.shape_q or tuple(k.shape) != self.shape_kv or tuple(v.shape) != self.shape_kv:
+            raise InvalidInputError(f"plan built for q{self.shape_q} kv{self.shape_kv}")
+        if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+            raise InvalidInputError("plan inputs must be bf16")
+        a = self.args
+        a.q, a.k, a.v = q.data_ptr(), k.data_ptr(), v.data_ptr()
+        a.q_stride_b, a.q_stride_h, a.q_stride_n = q.stride(0), q.stride(1), q.stride(2)
+        a.k_stride_b, a.k_stride_h, a.k_stride_n = k.stride(0), k.stride(1), k.stride(2)
+        a.v_stride_b, a.v_stride_h, a.v_stride_n = v.stride(0), v.stride(1), v.stride(2)
+        if reset_counters:
+            self.counters.zero_()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
+        return self.o
