@@ -3,10 +3,11 @@
 // One CTA owns NQ query tiles of 128 rows that share one kv head (two q heads
 // of a GQA group when NQ == 2) and streams the causally reachable 128-key
 // tiles of that kv head.  Warp roles:
-//   warps [0, 4*NQ)   softmax warpgroups, one per query tile; thread r owns
-//                     row r of its tile (TMEM lane r)
-//   warp 4*NQ         TMA producer (Q once, K every tile, V only when kept)
-//   warp 4*NQ+1       MMA issuer (tcgen05, single thread) + TMEM owner
+//   warps [0, 8*NQ)   softmax: 8 warps (256 threads) per query tile, two
+//                     threads per row (TMEM lane), each owning one 64-key
+//                     half of the 128-key tile (= one gate tile at b_n=64)
+//   warp 8*NQ         TMA producer (Q once, K every tile, V only when kept)
+//   warp 8*NQ+1       MMA issuer (tcgen05, single thread) + TMEM owner
 //
 // Per 128-key tile j and query tile s:
 //   QK:  S_s = Q_s K_j^T           tcgen05.mma SS, fp32 accumulator in TMEM
@@ -66,7 +67,7 @@ struct KCfg {
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = KT * D * 2;
   static constexpr int V_TILE = BN * D * 2;  // one gate tile of V
-  static constexpr int KS = CALIB ? 4 : (D == 128 ? 2 : 3);
+  static constexpr int KS = CALIB ? 3 : (D == 128 ? 2 : 3);
   static constexpr int VS = CALIB ? 0 : 65536 / V_TILE;  // slots of one V gate tile (64 KB ring)
   static constexpr int DQ = KS;              // decision ring depth (see producer)
   static constexpr int MAXA = 4096;          // calibration: max off-frontier gate tiles per row
@@ -77,7 +78,9 @@ struct KCfg {
   static constexpr int CAL_BYTES = CALIB ? NQ * MAXA * 4 : 0;
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
   static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + NQ * (3 + DQ);
-  static constexpr int OFF_DEC = OFF_BAR + NUM_BARS * 8;
+  static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8;                  // row max / vote exchange
+  static constexpr int XCH_BYTES = NQ * (2 * 2 * 128 * 4 + 16 * 4);
+  static constexpr int OFF_DEC = OFF_XCH + XCH_BYTES;
   static constexpr int OFF_TMEMPTR = OFF_DEC + NQ * DQ * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   // TMEM columns
@@ -85,16 +88,17 @@ struct KCfg {
   static constexpr int S_COL = CALIB ? 0 : NQ * D;
   static constexpr int TMEM_NEED = S_COL + NQ * KT;
   static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
-  static constexpr int NUM_THREADS = NQ * 128 + 64;
-  static constexpr int PRODUCER_WARP = NQ * 4;
-  static constexpr int MMA_WARP = NQ * 4 + 1;
+  static constexpr int SOFTMAX_WARPS = NQ * 8;  // two threads per row: 64-key column halves
+  static constexpr int NUM_THREADS = SOFTMAX_WARPS * 32 + 64;
+  static constexpr int PRODUCER_WARP = SOFTMAX_WARPS;
+  static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static_assert(CALIB || VS >= 2 * NH, "V ring must hold two tiles");
 };
 
 template <int D, int NH, int NQ, bool CALIB>
-__global__ void __launch_bounds__(NQ * 128 + 64, 1)
+__global__ void __launch_bounds__(NQ * 256 + 64, 1)
     bsfa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
   using C = KCfg<D, NH, NQ, CALIB>;
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&p_full[s], 8);
       mbar_init(&o_full[s], 1);
       for (int i = 0; i < DQ; ++i) mbar_init(&dec_full[s * DQ + i], 1);
     }
@@ -320,17 +324,24 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 4 * NQ) {
+  } else if (warp < C::SOFTMAX_WARPS) {
     // ======================= softmax warpgroups =======================
-    const int s = warp >> 2;
+    // Query tile s has 8 warps: warp quarter wq owns TMEM lanes [32wq, 32wq+32)
+    // (= rows), column half ch owns keys [64ch, 64ch+64) of each 128-key tile.
+    // With b_n = 64 a thread's half is exactly one gate tile.
+    const int s = warp >> 3;
     const int wq = warp & 3;
+    const int ch = (warp >> 2) & 1;
     const int r = wq * 32 + lane;  // row inside the query tile == TMEM lane
     const int hq = hq0 + s;
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const uint32_t s_tm = tmem + lane_off + C::S_COL + s * KT;
-    const uint32_t o_tm = tmem + lane_off + C::O_COL + s * D;
+    constexpr int DH = D / 2;  // O columns owned by this thread
+    const uint32_t o_tm = tmem + lane_off + C::O_COL + s * D + ch * DH;
     const uint32_t bar_id = 1 + s;
     const float sl2 = p.scale_log2;
+    float* xrow = reinterpret_cast<float*>(smem + C::OFF_XCH) + s * (2 * 2 * 128);  // [2 parity][2 half][128]
+    uint32_t* xwarp = reinterpret_cast<uint32_t*>(smem + C::OFF_XCH + NQ * 2 * 2 * 128 * 4) + s * 16;  // [2][8]
 
     float T = 0.f;
     if (!CALIB && p.gate_mode == kGateThreshold) {
@@ -338,72 +349,81 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
       T = p.thr[(long long)hq * p.thr_positions + pos];
     }
 
-    float m_ref = -INFINITY;  // raw (unscaled) running reference max
-    float l_sum = 0.f;
+    // Ping-pong between the two query tiles (NQ == 2): the softmax sections
+    // alternate (named barriers TURN0/TURN1, 512 threads each) so one tile's
+    // exponentials overlap the other tile's PV + QK on the tensor cores
+    // instead of both competing for the MUFUs and then both idling.
+    const uint32_t turn_mine = 3 + s, turn_other = 3 + (s ^ 1);
+    if (NQ == 2 && !CALIB && s == 1) named_bar_arrive(turn_other, 512);
+
+    float m_ref = -INFINITY;  // raw (unscaled) reference max of this row
+    float l_part = 0.f;       // row-sum of this thread's columns, relative to m_ref
     bool o_valid = false;
     unsigned long long kept_tiles = 0;
 
     for (int j = 0; j < ntiles; ++j) {
       mbar_wait(&s_full[s], j & 1);
+      if (NQ == 2 && !CALIB) named_bar_sync(turn_mine, 512);
       tc_fence_after();
-      uint32_t sv[KT];
-#pragma unroll
-      for (int c = 0; c < KT / 32; ++c) tmem_ld32(s_tm + c * 32, &sv[c * 32]);
+      uint32_t sv[64];
+      tmem_ld32(s_tm + ch * 64, &sv[0]);
+      tmem_ld32(s_tm + ch * 64 + 32, &sv[32]);
       tmem_wait_ld();
 
       const bool frontier = (j == qi);
       if (!CALIB) {
         if (frontier && p.causal) {
 #pragma unroll
-          for (int c = 0; c < KT; ++c)
-            if (c > r) sv[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < 64; ++c)
+            if (ch * 64 + c > r) sv[c] = __float_as_uint(-INFINITY);
         }
         if (!p.causal && (j + 1) * KT > p.valid_len) {
 #pragma unroll
-          for (int c = 0; c < KT; ++c)
-            if (j * KT + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < 64; ++c)
+            if (j * KT + ch * 64 + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
         }
       }
-      float rm[NH];
+      float pm;
+      {
+        float m0 = fmaxf(__uint_as_float(sv[0]), __uint_as_float(sv[1]));
+        float m1 = fmaxf(__uint_as_float(sv[2]), __uint_as_float(sv[3]));
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        float m0 = __uint_as_float(sv[h * BN]), m1 = __uint_as_float(sv[h * BN + 1]);
-        float m2 = __uint_as_float(sv[h * BN + 2]), m3 = __uint_as_float(sv[h * BN + 3]);
-#pragma unroll
-        for (int c = 4; c < BN; c += 4) {
-          m0 = fmaxf(m0, __uint_as_float(sv[h * BN + c]));
-          m1 = fmaxf(m1, __uint_as_float(sv[h * BN + c + 1]));
-          m2 = fmaxf(m2, __uint_as_float(sv[h * BN + c + 2]));
-          m3 = fmaxf(m3, __uint_as_float(sv[h * BN + c + 3]));
+        for (int c = 4; c < 64; c += 4) {
+          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])));
+          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])));
         }
-        rm[h] = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        pm = fmaxf(m0, m1);
       }
 
       if constexpr (CALIB) {
+        float m = pm;
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          float m = rm[h];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-          if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * NH + h], float_to_ordered(m * p.scale));
-        }
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * NH + (NH == 2 ? ch : 0)], float_to_ordered(m * p.scale));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
         continue;
       } else {
+        // ---- exchange row maxima and gate votes between the two column halves
+        const int par = j & 1;
+        const bool vote = (p.gate_mode == kGateThreshold) && (pm * p.scale > T);
+        const uint32_t wv = __ballot_sync(0xffffffffu, vote);
+        xrow[(par * 2 + ch) * 128 + r] = pm;
+        if (lane == 0) xwarp[par * 8 + ch * 4 + wq] = wv != 0u ? 1u : 0u;
+        named_bar_sync(bar_id, 256);
+        const float pm_other = xrow[(par * 2 + (ch ^ 1)) * 128 + r];
+        const uint32_t v0 = xwarp[par * 8 + 0] | xwarp[par * 8 + 1] | xwarp[par * 8 + 2] | xwarp[par * 8 + 3];
+        const uint32_t v1 = xwarp[par * 8 + 4] | xwarp[par * 8 + 5] | xwarp[par * 8 + 6] | xwarp[par * 8 + 7];
         uint32_t bits;
         if (frontier || p.gate_mode == kGateDense) {
           bits = HMASK;
         } else if (p.gate_mode == kGateFrontier) {
           bits = 0;
         } else {
-          bits = 0;
-#pragma unroll
-          for (int h = 0; h < NH; ++h)
-            bits |= named_bar_red_or(bar_id, 128, (rm[h] * p.scale > T) ? 1u : 0u) << h;
+          bits = (NH == 2) ? (v0 | (v1 << 1)) : (v0 | v1);
         }
-        if (r == 0) {
+        if (r == 0 && ch == 0) {
           const int di = s * DQ + (j % DQ);
           dec_words[di] = bits;
           mbar_arrive(&dec_full[di]);
@@ -419,13 +439,14 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[s]);
+          if (NQ == 2 && !(s == 1 && j == ntiles - 1)) named_bar_arrive(turn_other, 512);
           continue;
         }
 
-        float mx = -INFINITY;
-#pragma unroll
-        for (int h = 0; h < NH; ++h)
-          if ((bits >> h) & 1u) mx = fmaxf(mx, rm[h]);
+        const bool mine = (NH == 2) ? ((bits >> ch) & 1u) : true;
+        const bool theirs = (NH == 2) ? ((bits >> (ch ^ 1)) & 1u) : true;
+        float mx = mine ? pm : -INFINITY;
+        if (theirs) mx = fmaxf(mx, pm_other);
         const float m_new = fmaxf(m_ref, mx);
         const bool need = m_new > m_ref + p.rescale_raw;
         float alpha = 1.f;
@@ -435,36 +456,45 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
           alpha = ex2_approx((m_ref - m_new) * sl2);
           m_ref = m_new;
         }
-        const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
-
-        // P = exp(s - m) for kept gate tiles, packed bf16, written over S
-        float rs0 = 0.f, rs1 = 0.f;
+        if (mine) {
+          // P = exp2(s * scale*log2e - m * scale*log2e), bf16-packed over S
+          const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
+          const uint64_t sl2x2 = f2_pack(sl2, sl2);
+          const uint64_t negx2 = f2_pack(neg, neg);
+          uint64_t acc0 = 0, acc1 = 0;
+          uint32_t pk[32];
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          if ((bits >> h) & 1u) {
-            uint32_t pk[BN / 2];
-#pragma unroll
-            for (int c = 0; c < BN; c += 2) {
-              const float p0 = ex2_approx(fmaf(__uint_as_float(sv[h * BN + c]), sl2, neg));
-              const float p1 = ex2_approx(fmaf(__uint_as_float(sv[h * BN + c + 1]), sl2, neg));
-              rs0 += p0;
-              rs1 += p1;
-              pk[c / 2] = pack_bf16x2(p0, p1);
-            }
-#pragma unroll
-            for (int c = 0; c < BN / 2; c += 32) tmem_st32(s_tm + h * (BN / 2) + c, &pk[c]);
+          for (int c = 0; c < 64; c += 4) {
+            const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2x2, negx2);
+            const uint64_t x1 =
+                ffma2(f2_pack(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), sl2x2, negx2);
+            const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
+            const float p2 = ex2_approx(f2_lo(x1)), p3 = ex2_approx(f2_hi(x1));
+            acc0 = fadd2(acc0, f2_pack(p0, p1));
+            acc1 = fadd2(acc1, f2_pack(p2, p3));
+            pk[c / 2] = pack_bf16x2(p0, p1);
+            pk[c / 2 + 1] = pack_bf16x2(p2, p3);
           }
+          tmem_st32(s_tm + ch * 32, pk);
+          const uint64_t acc = fadd2(acc0, acc1);
+          l_part = l_part * alpha + (f2_lo(acc) + f2_hi(acc));
+        } else {
+          l_part = l_part * alpha;
         }
-        l_sum = l_sum * alpha + (rs0 + rs1);
 
         if (o_valid && __any_sync(0xffffffffu, need)) {
+          const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
-          for (int c = 0; c < D; c += 32) {
+          for (int c = 0; c < DH; c += 32) {
             uint32_t ov[32];
             tmem_ld32(o_tm + c, ov);
             tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            for (int e = 0; e < 32; e += 2) {
+              const uint64_t t = fmul2(f2_pack(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])), ax2);
+              ov[e] = __float_as_uint(f2_lo(t));
+              ov[e + 1] = __float_as_uint(f2_hi(t));
+            }
             tmem_st32(o_tm + c, ov);
           }
         }
@@ -472,6 +502,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
+        if (NQ == 2 && !(s == 1 && j == ntiles - 1)) named_bar_arrive(turn_other, 512);
         o_valid = true;
       }
     }
@@ -479,18 +510,18 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
     if constexpr (CALIB) {
       // ---- order statistics of this row of tile maxima (calibration.py:116-153)
       const int A = ntiles * NH;
-      const int t = r;
-      named_bar_sync(bar_id, 128);
+      const int t = ch * 128 + r;  // 0..255
+      named_bar_sync(bar_id, 256);
       int* vals = cvals + s * C::MAXA;
       if (p.c_maxima) {
         float* out = p.c_maxima + ((long long)hq * p.num_q_tiles + qi) * p.gate_cols;
-        for (int x = t; x < A; x += 128) out[x] = ordered_to_float(vals[x]);
+        for (int x = t; x < A; x += 256) out[x] = ordered_to_float(vals[x]);
       }
       int n2 = 1;
       while (n2 < A) n2 <<= 1;
       for (int kk = 2; kk <= n2; kk <<= 1) {
         for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (int x = t; x < n2; x += 128) {
+          for (int x = t; x < n2; x += 256) {
             const int y = x ^ jj;
             if (y > x) {
               const int a = vals[x], c = vals[y];
@@ -501,7 +532,7 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
               }
             }
           }
-          named_bar_sync(bar_id, 128);
+          named_bar_sync(bar_id, 256);
         }
       }
       if (t < p.c_num_levels) {
@@ -530,18 +561,22 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
       }
     } else {
       // ---- epilogue: O / l -> bf16, lse = m*scale + ln(l)   (engine.py:178-182)
+      xrow[(2 * 2 - 1 - ch) * 128 + r] = l_part;  // slots [1][*] of the exchange buffer are free now
       mbar_wait(&o_full[s], 0);
       tc_fence_after();
+      named_bar_sync(bar_id, 256);
+      const float l_sum = l_part + xrow[(2 + ch) * 128 + r];
       const float inv_l = 1.f / l_sum;
       bool bad = !(l_sum > 0.f);
       const int row = qi * 128 + r;
-      __nv_bfloat16* orow = p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
+      __nv_bfloat16* orow =
+          p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + ch * DH;
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
+      for (int c = 0; c < DH; c += 32) {
         uint32_t ov[32];
         tmem_ld32(o_tm + c, ov);
         tmem_wait_ld();
-        if (p.inject_fault && qi == 0 && r == 0 && c == 0)
+        if (p.inject_fault && qi == 0 && r == 0 && ch == 0 && c == 0)
           ov[0] = __float_as_uint(__uint_as_float(ov[0]) + l_sum);  // +1.0 on O[0][0]
         uint32_t pk[16];
 #pragma unroll
@@ -554,9 +589,9 @@ __global__ void __launch_bounds__(NQ * 128 + 64, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
       }
-      p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * p.scale + logf(l_sum);
+      if (ch == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * p.scale + logf(l_sum);
       if (bad && p.status) atomicOr(p.status, 1);
-      if (r == 0 && p.counters) {
+      if (r == 0 && ch == 0 && p.counters) {
         atomicAdd(&p.counters[0], (unsigned long long)ntiles * NH);
         atomicAdd(&p.counters[1], kept_tiles);
       }

@@ -1,0 +1,100 @@
+"""Head sharding + output all-gather, exercised with world_size 2 on gloo (CPU).
+
+The per-rank compute is the CPU oracle (tests may use it); what is tested is
+the partition (which q/kv heads and threshold rows a rank owns) and the
+gather layout, i.e. the multi-GPU logic of ``distributed.py`` minus the
+kernel itself.
+"""
+
+import os
+import socket
+from dataclasses import dataclass
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2512_07011_b200.distributed import HeadShard, gather_heads, shard_heads, sharded_attention
+from paper_2512_07011_b200.errors import ConfigurationError
+
+
+def test_shard_heads_partition():
+    assert shard_heads(32, 8, 8, 3) == HeadShard(3, 8, 12, 16, 3, 4)
+    assert shard_heads(32, 8, 2, 1) == HeadShard(1, 2, 16, 32, 4, 8)
+    cover = sorted(h for r in range(4) for h in range(*(lambda s: (s.q_lo, s.q_hi))(shard_heads(32, 8, 4, r))))
+    assert cover == list(range(32))
+    with pytest.raises(ConfigurationError):
+        shard_heads(32, 8, 3, 0)
+
+
+@dataclass
+class _Res:
+    o: torch.Tensor
+
+
+def _oracle_compute(q, k, v, thresholds=None, layer=0, k_level=None, head_offset=0, **kw):
+    from oracle import bsfa_oracle as orc
+    b, hq, n, d = q.shape
+    g = hq // k.shape[1]
+    lvl = thresholds.level_index(k_level)
+    out = torch.empty_like(q)
+    for bi in range(b):
+        for h in range(hq):
+            thr = thresholds.values[lvl, layer, head_offset + h]
+            o, _, _ = orc.flash_forward(q[bi, h].numpy(), k[bi, h // g].numpy(), v[bi, h // g].numpy(), True,
+                                        128, 64, orc.threshold_gate(thr))
+            out[bi, h] = torch.from_numpy(o)
+    return _Res(out)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q, k, v, thr, expected, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, full = sharded_attention(q, k, v, rank=rank, world=world, thresholds=thr, layer=1, k_level=4,
+                                    gather=True, compute=_oracle_compute)
+        err = float((full - expected).abs().max())
+        result_q.put((rank, tuple(full.shape), err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_two_rank_gather_matches_single_process(batch):
+    import paper_2512_07011_b200 as bsfa
+    rng = np.random.default_rng(batch)
+    hq, hkv, n, d = 4, 2, 256, 16
+    q = torch.from_numpy(rng.standard_normal((batch, hq, n, d)).astype(np.float32))
+    k = torch.from_numpy(rng.standard_normal((batch, hkv, n, d)).astype(np.float32))
+    v = torch.from_numpy(rng.standard_normal((batch, hkv, n, d)).astype(np.float32))
+    vals = rng.uniform(0.5, 1.0, size=(1, 2, hq, 2)).astype(np.float32)
+    thr = bsfa.ThresholdTensor(values=vals, k_levels=(4,), n_max=256, b_m=128, b_n=64)
+    expected = _oracle_compute(q, k, v, thresholds=thr, layer=1, k_level=4).o
+    ctx = mp.get_context("spawn")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, k, v, thr, expected, result_q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    results = sorted(result_q.get(timeout=10) for _ in range(2))
+    for rank, shape, err in results:
+        assert shape == (batch, hq, n, d)
+        assert err == 0.0, (rank, err)
+
+
+def test_gather_single_rank_is_identity():
+    x = torch.randn(1, 2, 8, 4)
+    assert gather_heads(x, 1) is x
