@@ -13,7 +13,8 @@ import threading
 
 from .errors import BsfaError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
+LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
 ABI_VERSION = 1
 

@@ -10,6 +10,10 @@
 #include "../../include/bsfa_b200.h"
 #include "bsfa_kernel.cuh"
 
+#ifndef BSFA_TPR_D128
+#define BSFA_TPR_D128 4
+#endif
+
 using namespace bsfa;
 
 namespace {
@@ -71,11 +75,16 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
-template <int D, int NH, int NQ, bool CALIB>
+// Threads per softmax row: 4 at d=128 (more warps to hide the per-tile
+// latency chain), 2 at d=64 (keeps 32 O columns per thread).
+template <int D>
+constexpr int kTPR = D == 128 ? BSFA_TPR_D128 : 2;
+
+template <int D, int NH, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  using C = KCfg<D, NH, NQ, CALIB>;
-  auto kern = bsfa_kernel<D, NH, NQ, CALIB>;
+  using C = KCfg<D, NH, CALIB, kTPR<D>>;
+  auto kern = bsfa_kernel<D, NH, CALIB, kTPR<D>>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -90,20 +99,16 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 }
 
 template <bool CALIB>
-int dispatch(int d, int nh, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+int dispatch(int d, int nh, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& p, int grid, cudaStream_t st) {
-#define BSFA_CASE(D_, NH_, NQ_) \
-  if (d == D_ && nh == NH_ && nq == NQ_) return launch<D_, NH_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
-  BSFA_CASE(64, 1, 1)
-  BSFA_CASE(64, 1, 2)
-  BSFA_CASE(64, 2, 1)
-  BSFA_CASE(64, 2, 2)
-  BSFA_CASE(128, 1, 1)
-  BSFA_CASE(128, 1, 2)
-  BSFA_CASE(128, 2, 1)
-  BSFA_CASE(128, 2, 2)
+#define BSFA_CASE(D_, NH_) \
+  if (d == D_ && nh == NH_) return launch<D_, NH_, CALIB>(tq, tk, tv, p, grid, st);
+  BSFA_CASE(64, 1)
+  BSFA_CASE(64, 2)
+  BSFA_CASE(128, 1)
+  BSFA_CASE(128, 2)
 #undef BSFA_CASE
-  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d gate tiles/MMA tile=%d q tiles/CTA=%d", d, nh, nq);
+  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d gate tiles per MMA tile=%d", d, nh);
 }
 
 int check_tiles(int b_m, int b_n) {
@@ -184,11 +189,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.counters = a->counters;
   p.status = a->status;
 
-  const int nq = (p.group % 2 == 0) ? 2 : 1;
   const int nh = 128 / a->b_n;
-  const long long grid = (long long)a->batch * a->heads_kv * (p.group / nq) * p.num_q_tiles;
+  const long long grid = (long long)a->batch * a->heads_q * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
-  return dispatch<false>(d, nh, nq, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch<false>(d, nh, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
@@ -200,8 +204,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
-  if (a->seq_len / a->b_n > KCfg<64, 2, 1, true>::MAXA)
-    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, 1, true>::MAXA);
+  if (a->seq_len / a->b_n > KCfg<64, 2, true, 2>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, true, 2>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
   if (a->seq_len / a->b_m > a->num_positions)
@@ -243,10 +247,9 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.c_ties = a->tie_counts;
   p.c_maxima = a->block_maxima;
 
-  const int nq = (p.group % 2 == 0) ? 2 : 1;
   const int nh = 128 / a->b_n;
-  const int grid = a->heads_kv * (p.group / nq) * p.num_q_tiles;
-  return dispatch<true>(d, nh, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+  const int grid = a->heads_q * p.num_q_tiles;
+  return dispatch<true>(d, nh, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
