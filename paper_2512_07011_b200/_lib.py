@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "bsfa_last_error",
     "bsfa_device_supported",
     "bsfa_fwd",
+    "bsfa_debug_trace",
     "bsfa_calib_blockmax",
     "bsfa_calib_finalize",
 )
@@ -121,6 +122,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.bsfa_device_supported.argtypes = []
         lib.bsfa_fwd.restype = ctypes.c_int
         lib.bsfa_fwd.argtypes = [ctypes.POINTER(FwdArgs), ctypes.c_void_p]
+        lib.bsfa_debug_trace.restype = ctypes.c_int
+        lib.bsfa_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.bsfa_calib_blockmax.restype = ctypes.c_int
         lib.bsfa_calib_blockmax.argtypes = [ctypes.POINTER(CalibArgs), ctypes.c_void_p]
         lib.bsfa_calib_finalize.restype = ctypes.c_int

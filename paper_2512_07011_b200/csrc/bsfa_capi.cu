@@ -10,15 +10,13 @@
 #include "../../include/bsfa_b200.h"
 #include "bsfa_kernel.cuh"
 
-#ifndef BSFA_TPR_D128
-#define BSFA_TPR_D128 4
-#endif
-
 using namespace bsfa;
 
 namespace {
 
 thread_local std::string g_last_error;
+long long* g_trace = nullptr;  // debug timeline buffer (bsfa_debug_trace)
+int g_trace_cta = -1;
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -75,16 +73,11 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
-// Threads per softmax row: 4 at d=128 (more warps to hide the per-tile
-// latency chain), 2 at d=64 (keeps 32 O columns per thread).
-template <int D>
-constexpr int kTPR = D == 128 ? BSFA_TPR_D128 : 2;
-
 template <int D, int NH, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  using C = KCfg<D, NH, CALIB, kTPR<D>>;
-  auto kern = bsfa_kernel<D, NH, CALIB, kTPR<D>>;
+  using C = KCfg<D, NH, CALIB>;
+  auto kern = bsfa_kernel<D, NH, CALIB>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -132,6 +125,12 @@ int bsfa_device_supported(void) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
   return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+}
+
+int bsfa_debug_trace(long long* dev_buf, int cta) {
+  g_trace = dev_buf;
+  g_trace_cta = cta;
+  return BSFA_OK;
 }
 
 int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
@@ -185,6 +184,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.o_sh = a->o_stride_h;
   p.o_sn = a->o_stride_n;
   p.lse = a->lse;
+  p.trace = g_trace;
+  p.trace_cta = g_trace_cta;
   p.decisions = a->decisions;
   p.counters = a->counters;
   p.status = a->status;
@@ -204,8 +205,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
-  if (a->seq_len / a->b_n > KCfg<64, 2, true, 2>::MAXA)
-    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, true, 2>::MAXA);
+  if (a->seq_len / a->b_n > KCfg<64, 2, true>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, true>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
   if (a->seq_len / a->b_m > a->num_positions)

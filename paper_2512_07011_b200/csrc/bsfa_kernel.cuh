@@ -2,33 +2,48 @@
 //
 // One CTA owns one query tile (128 rows of one q head, query block i) and
 // streams the reachable 128-key tiles of that head's kv head.  Warp roles:
-//   warps 0..4TPR-1  softmax: TPR threads per row (TMEM lane = row), each
-//                    owning 128/TPR consecutive keys of every 128-key tile
-//   warp 4TPR        TMA producer for Q and K (K ring, unconditional)
-//   warp 4TPR+1      tcgen05 issuer (single thread) + TMEM owner
-//   warp 4TPR+2      TMA producer for V: fetches a V gate tile only when the
-//                    gate kept it (decision ring from the softmax warps)
-// TMEM holds O (fp32, d columns) and an NS-deep ring of S tiles (fp32, 128
-// columns); P (bf16) is written over its S slot and read by the PV MMA (A
-// operand from TMEM).  QK^T for tile j+NS is issued right after PV of tile j,
-// so the score tiles are computed ahead of the softmax.
+//   warps 0..7   softmax, two groups of 4 warps.  Group g owns the key tiles
+//                j = g (mod 2) of this query tile: thread r of a group owns
+//                row r (TMEM lane r) over all 128 keys of the tile, keeps its
+//                own running max / sum and accumulates into its own O slot.
+//                The two partial states are merged in the epilogue (the same
+//                rescale-and-add the online softmax does between tiles).
+//   warp 8       TMA producer for Q and K (K ring, unconditional)
+//   warp 9       tcgen05 issuer (warp-convergent, one elected lane) + TMEM owner
+//   warp 10      TMA producer for V: fetches a V gate tile only when the
+//                gate kept it (decision ring from the softmax groups)
+// TMEM: O_0, O_1 (fp32, d columns each) and one S slot (fp32, 128 columns)
+// per group; P (bf16) is written over the slot and read by the PV MMA (A
+// operand from TMEM).  While one group runs its exponentials the tensor
+// cores run the other group's PV and next QK^T.
 //
-// Per 128-key tile j:
-//   QK:   S = Q K_j^T                     8 x tcgen05.mma 128x128x16 (SS)
+// Per 128-key tile j (group g = j mod 2):
+//   QK:   S_g = Q K_j^T                   8 x tcgen05.mma 128x128x16 (SS)
 //   gate: per gate tile, OR over rows of (rowmax * scale > T) == the
 //         reference's tile.s_max > T (gates.py:77-78, engine.py:30-38)
 //   skip: no V TMA, no exp, no PV MMA, no statistics update (engine.py:172-174)
-//   keep: online softmax (engine.py:57-68), lazily rescaled O, O += P V_j
+//   keep: online softmax (engine.py:57-68), lazily rescaled O_g, O_g += P V_j
 // Calibration (CALIB) runs the same QK front end over the off-frontier prefix
 // j < A_p only (calibration.py:108-115) and reduces tile maxima in smem.
 #pragma once
 
 #include "ptx.cuh"
 
+// Fraction of exponentials computed by polynomial on the FMA pipe instead of
+// the MUFU: 0 = none, 1 = 1/4, 2 = 1/2.
+#ifndef BSFA_EXP_EMU
+#define BSFA_EXP_EMU 1
+#endif
+// Softmax groups take turns (named-barrier hand-off) so each group's
+// exponentials run while the other group's PV/QK are on the tensor cores,
+// instead of both groups sharing the MUFUs and then both waiting.
+#ifndef BSFA_TURNS
+#define BSFA_TURNS 1
+#endif
+
 namespace bsfa {
 
 enum : int { kGateThreshold = 0, kGateDense = 1, kGateFrontier = 2 };
-constexpr uint32_t kRescaleFlag = 0x80000000u;  // decision-word bit: O rescale before this tile's PV
 
 struct KernelParams {
   int batch, heads_q, heads_kv, group;
@@ -60,9 +75,16 @@ struct KernelParams {
   int* c_pos;
   unsigned long long* c_ties;
   float* c_maxima;
+  // debug: per-tile clock64 timestamps of one CTA (bsfa_debug_trace)
+  long long* trace;
+  int trace_cta;
 };
 
-template <int D, int NH, bool CALIB, int TPR>
+// trace slots: trace[ev * kTraceTiles + j]
+constexpr int kTraceTiles = 4096;
+enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvIssued = 4, kEvSReadyG1 = 5 };
+
+template <int D, int NH, bool CALIB>
 struct KCfg {
   static constexpr int KT = 128;             // keys per MMA tile
   static constexpr int BN = KT / NH;         // gate tile width (reference b_n)
@@ -70,10 +92,11 @@ struct KCfg {
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = KT * D * 2;
   static constexpr int V_TILE = BN * D * 2;  // one gate tile of V
-  static constexpr int NS = CALIB ? 4 : 3;   // S ring depth in TMEM
-  static constexpr int KS = CALIB ? 4 : 2;   // K ring depth in smem (QK issue is paced by the S ring)
-  static constexpr int VS = CALIB ? 0 : (D == 128 ? 6 : 12) / (3 - NH);  // V gate-tile slots
-  static constexpr int DQ = 8;               // decision ring depth (>= NS)
+  static constexpr int NG = 2;               // softmax groups (alternate key tiles)
+  static constexpr int NS = CALIB ? 4 : NG;  // S slots in TMEM (slot = tile mod NS)
+  static constexpr int KS = CALIB ? 4 : (D == 128 ? 2 : 3);  // K ring depth in smem
+  static constexpr int VS = CALIB ? 0 : (D == 128 ? 6 : 12) / (3 - NH);  // V gate-tile slots (96 KB ring)
+  static constexpr int DQ = 8;               // decision ring depth
   static constexpr int MAXA = 4096;          // calibration: max off-frontier gate tiles per row
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_TILE;
@@ -81,37 +104,33 @@ struct KCfg {
   static constexpr int OFF_CAL = OFF_V + VS * V_TILE;
   static constexpr int CAL_BYTES = CALIB ? MAXA * 4 : 0;
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 2 * NS + 2 * DQ + 3;
-  static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8;  // [2 parity][TPR][128] f32 + [2][16] u32 + [TPR][128] f32
-  static constexpr int XCH_BYTES = 2 * TPR * 128 * 4 + 2 * 16 * 4 + TPR * 128 * 4;
+  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 2 * NS + 2 * DQ + 1;
+  static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8;  // votes u32 [NG][2][4], final (m,l) f32 [NG][128][2]
+  static constexpr int XCH_BYTES = NG * 2 * 4 * 4 + NG * 128 * 8;
   static constexpr int OFF_DEC = OFF_XCH + XCH_BYTES;
   static constexpr int OFF_TMEMPTR = OFF_DEC + DQ * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   // TMEM columns
-  static constexpr int O_COL = 0;
-  static constexpr int S_COL = CALIB ? 0 : D;
+  static constexpr int S_COL = CALIB ? 0 : NG * D;  // O_g at g*D
   static constexpr int TMEM_NEED = S_COL + NS * KT;
   static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
-  static constexpr int CW = 128 / TPR;       // key columns per softmax thread
-  static constexpr int SOFTMAX_WARPS = 4 * TPR;
+  static constexpr int SOFTMAX_WARPS = 4 * NG;
   static constexpr int KPROD_WARP = SOFTMAX_WARPS;
   static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static constexpr int VPROD_WARP = SOFTMAX_WARPS + 2;
   static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 3) * 32;
-  static_assert(TPR == 2 || TPR == 4, "2 or 4 threads per row");
-  static_assert(D / TPR >= 32, "O columns per thread must be a multiple of 32");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(TMEM_NEED <= 512, "TMEM budget");
-  static_assert(CALIB || VS >= NH * NS, "V ring must cover the S ring");
+  static_assert(CALIB || VS >= 2 * NH, "V ring must hold two tiles");
   static_assert(DQ >= NS && DQ >= KS, "decision ring depth");
 };
 
-template <int D, int NH, bool CALIB, int TPR>
-__global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
+template <int D, int NH, bool CALIB>
+__global__ void __launch_bounds__(11 * 32, 1)
     bsfa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = KCfg<D, NH, CALIB, TPR>;
-  constexpr int KT = C::KT, BN = C::BN, KS = C::KS, VS = C::VS, NS = C::NS, DQ = C::DQ;
+  using C = KCfg<D, NH, CALIB>;
+  constexpr int KT = C::KT, BN = C::BN, KS = C::KS, VS = C::VS, NS = C::NS, DQ = C::DQ, NG = C::NG;
   constexpr uint32_t HMASK = (1u << NH) - 1u;
 
   extern __shared__ uint8_t smem_raw[];
@@ -131,13 +150,10 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
   uint64_t* dec_full = p_full + NS;
   uint64_t* dec_empty = dec_full + DQ;
   uint64_t* o_full = dec_empty + DQ;
-  uint64_t* o_quiet = o_full + 1;     // MMA commit: every issued MMA has landed (rescale may touch O)
-  uint64_t* o_rescaled = o_full + 2;  // softmax warps: O rescaled, PV may resume
   volatile uint32_t* dec_words = reinterpret_cast<volatile uint32_t*>(smem + C::OFF_DEC);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
-  const uint32_t xch_row = smem_u32(smem + C::OFF_XCH);         // f32 [2][TPR][128]  partial row maxima
-  const uint32_t xch_vote = xch_row + 2 * TPR * 128 * 4;        // u32 [2][16]        per-warp votes
-  const uint32_t xch_l = xch_vote + 2 * 16 * 4;                 // f32 [TPR][128]     partial row sums
+  const uint32_t xch_vote = smem_u32(smem + C::OFF_XCH);  // u32 [NG][2][4] per-warp gate votes
+  const uint32_t xch_fin = xch_vote + NG * 2 * 4 * 4;      // f32 [NG][128][2] final (m, l) per row
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -167,15 +183,13 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], C::SOFTMAX_WARPS);
+      mbar_init(&p_full[i], 4);  // the 4 warps of the owning group
     }
     for (int i = 0; i < DQ; ++i) {
       mbar_init(&dec_full[i], 1);
       mbar_init(&dec_empty[i], 1);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_quiet, 1);
-    mbar_init(o_rescaled, C::SOFTMAX_WARPS);
     fence_mbarrier_init();
   }
   if constexpr (CALIB) {
@@ -257,13 +271,7 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
         mbar_wait(&k_full[st], (t / KS) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + C::S_COL + (t % NS) * KT;
-        const uint64_t dk = dk0 + uint64_t((st * C::K_TILE) >> 4);
-#pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_ss_w(d_tmem, dq0 + uint64_t((c * 128 * 128 + kk * 32) >> 4),
-                      dk + uint64_t((c * KT * 128 + kk * 32) >> 4), IDESC_QK, (c | kk) != 0 ? 1u : 0u);
+        umma_qk_tile_w<D>(d_tmem, dq0, dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
         umma_commit_w(&s_full[t % NS]);
         umma_commit_w(&k_empty[st]);
       };
@@ -272,21 +280,15 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
       for (int t = 0; t < pre; ++t) issue_qk(t);
 
       unsigned long long vcount = 0;
-      uint32_t o_started = 0;
-      uint32_t n_rescale = 0;
+      uint32_t o_started = 0;  // bit g: O_g holds a partial sum
       for (int j = 0; j < ntiles; ++j) {
         const int sb = j % NS;
         mbar_wait(&p_full[sb], (j / NS) & 1);
+        const bool tr = p.trace && (int)blockIdx.x == p.trace_cta && lane == 0 && j < kTraceTiles;
+        if (tr) p.trace[kEvPSeen * kTraceTiles + j] = clock64();
         if constexpr (!CALIB) {
-          const uint32_t word = __shfl_sync(0xffffffffu, dec_words[j % DQ], 0);
-          const uint32_t bits = word & HMASK;
-          if (word & kRescaleFlag) {
-            // the softmax warps rescale O in TMEM: let every in-flight MMA land,
-            // then hold PV_j until they are done
-            umma_commit_w(o_quiet);
-            mbar_wait(o_rescaled, n_rescale & 1);
-            ++n_rescale;
-          }
+          const int og = j % NG;
+          const uint32_t bits = __shfl_sync(0xffffffffu, dec_words[j % DQ], 0) & HMASK;
           const uint32_t p_tmem = tmem + C::S_COL + sb * KT;
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
@@ -297,10 +299,10 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
               tc_fence_after();
               const uint64_t dv = dv0 + uint64_t((slot * C::V_TILE) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < BN / 16; ++kk) {
-                umma_ts_w(tmem + C::O_COL, p_tmem + (h * BN + kk * 16) / 2, dv + uint64_t((kk * 16 * 128) >> 4),
-                          IDESC_PV, o_started);
-                o_started = 1;
+              for (int q = 0; q < BN / 64; ++q) {  // 64 keys per batch (1 for b_n=64, 2 for b_n=128)
+                umma_pv64_w(tmem + og * D, p_tmem + (h * BN + q * 64) / 2, dv + uint64_t(q * 512), IDESC_PV,
+                            (o_started >> og) & 1u);
+                o_started |= 1u << og;
               }
               umma_commit_w(&v_empty[slot]);
             }
@@ -309,24 +311,22 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
         } else {
           tc_fence_after();
         }
-        if (j + NS < ntiles) issue_qk(j + NS);  // reuses S slot sb, ordered after PV_j
+        // QK_{j+NS} reuses slot sb; issued after PV_j, so its commit also
+        // certifies that every earlier PV into O_{j mod NG} has landed.
+        if (j + NS < ntiles) issue_qk(j + NS);
+        if (tr) p.trace[kEvIssued * kTraceTiles + j] = clock64();
       }
     }
     __syncwarp();
   } else if (warp < C::SOFTMAX_WARPS) {
-    // ======================= softmax =======================
-    // TPR threads per row: warp quarter wq owns TMEM lanes [32wq, 32wq+32),
-    // column chunk cq owns keys [CW*cq, CW*cq + CW) of every 128-key tile.
-    constexpr int CW = C::CW;
-    constexpr int NTHR = 128 * TPR;
+    // ======================= softmax groups =======================
+    const int grp = warp >> 2;     // key tiles j = grp (mod NG)
     const int wq = warp & 3;
-    const int cq = warp >> 2;
-    const int gh = (NH == 2) ? (cq * CW) / 64 : 0;  // gate tile holding this chunk
-    const int r = wq * 32 + lane;                   // row inside the query tile == TMEM lane
+    const int r = wq * 32 + lane;  // row inside the query tile == TMEM lane
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    constexpr int DH = D / TPR;  // O columns owned by this thread
-    const uint32_t o_tm = tmem + lane_off + C::O_COL + cq * DH;
+    const uint32_t o_tm = tmem + lane_off + grp * D;  // this group's O slot
     const float sl2 = p.scale_log2;
+    const uint32_t vote_base = xch_vote + grp * 2 * 4 * 4;
 
     float T = 0.f;
     if (!CALIB && p.gate_mode == kGateThreshold) {
@@ -334,98 +334,93 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
       T = p.thr[(long long)hq * p.thr_positions + pos];
     }
 
-    float m_ref = -INFINITY;  // raw (unscaled) reference max of this row
-    float l_part = 0.f;       // row sum over this thread's columns, relative to m_ref
-    bool o_valid = false;
-    uint32_t n_rescale = 0;
+    constexpr bool kTurns = !CALIB && BSFA_TURNS;
+    const uint32_t turn_mine = 5 + grp, turn_other = 5 + (grp ^ 1);
+    if (kTurns && grp == 1) named_bar_arrive(turn_other, 256);  // group 0 goes first
+
+    float m_ref = -INFINITY;  // raw (unscaled) reference max of this row over this group's kept tiles
+    float l_sum = 0.f;        // row sum relative to m_ref
+    bool o_valid = false;     // group-uniform: O_g holds data
     unsigned long long kept_tiles = 0;
 
-    for (int j = 0; j < ntiles; ++j) {
+    for (int j = grp; j < ntiles; j += NG) {
       const int sb = j % NS;
+      const int use = j / NS;
       const uint32_t s_row = tmem + lane_off + C::S_COL + sb * KT;
-      mbar_wait(&s_full[sb], (j / NS) & 1);
+      mbar_wait(&s_full[sb], use & 1);
+      const bool tr = p.trace && (int)blockIdx.x == p.trace_cta && r == 0 && j < kTraceTiles;
+      if (tr) p.trace[kEvSReady * kTraceTiles + j] = clock64();
+      if (kTurns) named_bar_sync(turn_mine, 256);
       tc_fence_after();
-      uint32_t sv[CW];
+      uint32_t sv[KT];
 #pragma unroll
-      for (int c = 0; c < CW; c += 32) tmem_ld32(s_row + cq * CW + c, &sv[c]);
+      for (int c = 0; c < KT; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
 
       const bool frontier = (j == qi);
       if (!CALIB) {
         if (frontier && p.causal) {
 #pragma unroll
-          for (int c = 0; c < CW; ++c)
-            if (cq * CW + c > r) sv[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < KT; ++c)
+            if (c > r) sv[c] = __float_as_uint(-INFINITY);
         }
         if (!p.causal && (j + 1) * KT > p.valid_len) {
 #pragma unroll
-          for (int c = 0; c < CW; ++c)
-            if (j * KT + cq * CW + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < KT; ++c)
+            if (j * KT + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
         }
       }
-      float pm;
-      {
-        float m0 = fmaxf(__uint_as_float(sv[0]), __uint_as_float(sv[1]));
-        float m1 = fmaxf(__uint_as_float(sv[2]), __uint_as_float(sv[3]));
-        float m2 = fmaxf(__uint_as_float(sv[4]), __uint_as_float(sv[5]));
-        float m3 = fmaxf(__uint_as_float(sv[6]), __uint_as_float(sv[7]));
+      float rm[NH];  // row max per gate tile
 #pragma unroll
-        for (int c = 8; c < CW; c += 8) {
-          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])));
-          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])));
-          m2 = fmaxf(m2, fmaxf(__uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5])));
-          m3 = fmaxf(m3, fmaxf(__uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7])));
+      for (int h = 0; h < NH; ++h) {
+        float m0 = fmaxf(__uint_as_float(sv[h * BN]), __uint_as_float(sv[h * BN + 1]));
+        float m1 = fmaxf(__uint_as_float(sv[h * BN + 2]), __uint_as_float(sv[h * BN + 3]));
+        float m2 = fmaxf(__uint_as_float(sv[h * BN + 4]), __uint_as_float(sv[h * BN + 5]));
+        float m3 = fmaxf(__uint_as_float(sv[h * BN + 6]), __uint_as_float(sv[h * BN + 7]));
+#pragma unroll
+        for (int c = 8; c < BN; c += 8) {
+          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[h * BN + c]), __uint_as_float(sv[h * BN + c + 1])));
+          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[h * BN + c + 2]), __uint_as_float(sv[h * BN + c + 3])));
+          m2 = fmaxf(m2, fmaxf(__uint_as_float(sv[h * BN + c + 4]), __uint_as_float(sv[h * BN + c + 5])));
+          m3 = fmaxf(m3, fmaxf(__uint_as_float(sv[h * BN + c + 6]), __uint_as_float(sv[h * BN + c + 7])));
         }
-        pm = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        rm[h] = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
       }
 
       if constexpr (CALIB) {
-        float m = pm;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-        if (lane == 0) atomicMax(&cvals[j * NH + gh], float_to_ordered(m * p.scale));
+        for (int h = 0; h < NH; ++h) {
+          float m = rm[h];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+          if (lane == 0) atomicMax(&cvals[j * NH + h], float_to_ordered(m * p.scale));
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
         continue;
       } else {
-        // ---- exchange partial row maxima and gate votes between the chunks
-        const int par = j & 1;
-        const bool vote = (p.gate_mode == kGateThreshold) && (pm * p.scale > T);
-        const uint32_t wv = __ballot_sync(0xffffffffu, vote);
-        // conservative rescale request: this chunk's max outgrows the reference
-        const uint32_t wr = __ballot_sync(0xffffffffu, o_valid && pm > m_ref + p.rescale_raw);
-        sts_f32(xch_row + ((par * TPR + cq) * 128 + r) * 4, pm);
-        if (lane == 0) sts_u32(xch_vote + (par * 16 + warp) * 4, (wv != 0u ? 1u : 0u) | (wr != 0u ? 2u : 0u));
-        named_bar_sync(1, NTHR);
-        float pq[TPR];
-#pragma unroll
-        for (int q = 0; q < TPR; ++q) pq[q] = (q == cq) ? pm : lds_f32(xch_row + ((par * TPR + q) * 128 + r) * 4);
-        uint32_t vw[TPR];  // OR of the 4 warp votes of chunk q
-#pragma unroll
-        for (int q = 0; q < TPR; ++q) {
-          const uint4 v4 = lds_u128(xch_vote + (par * 16 + 4 * q) * 4);
-          vw[q] = v4.x | v4.y | v4.z | v4.w;
-        }
-        uint32_t vote_h0 = 0, vote_h1 = 0, rq = 0;
-#pragma unroll
-        for (int q = 0; q < TPR; ++q) {
-          if ((q * CW) / 64 == 0) vote_h0 |= vw[q] & 1u; else vote_h1 |= vw[q] & 1u;
-          rq |= vw[q] & 2u;
-        }
+        // ---- gate: OR over the group's 128 rows of (rowmax * scale > T)
         uint32_t bits;
         if (frontier || p.gate_mode == kGateDense) {
           bits = HMASK;
         } else if (p.gate_mode == kGateFrontier) {
           bits = 0;
         } else {
-          bits = (NH == 2) ? (vote_h0 | (vote_h1 << 1)) : (vote_h0 | vote_h1);
+          uint32_t wv = 0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) wv |= (__ballot_sync(0xffffffffu, rm[h] * p.scale > T) != 0u ? 1u : 0u) << h;
+          const uint32_t par = use & 1;
+          if (lane == 0) sts_u32(vote_base + (par * 4 + wq) * 4, wv);
+          named_bar_sync(1 + grp, 128);
+          const uint4 v4 = lds_u128(vote_base + par * 4 * 4);
+          bits = (v4.x | v4.y | v4.z | v4.w) & HMASK;
         }
-        const bool do_rescale = rq != 0u && bits != 0u;
-        if (warp == 0 && lane == 0) {
+        if (tr) p.trace[kEvVoted * kTraceTiles + j] = clock64();
+        if (r == 0) {
           const int di = j % DQ;
           mbar_wait(&dec_empty[di], ((j / DQ) & 1) ^ 1);
-          dec_words[di] = bits | (do_rescale ? kRescaleFlag : 0u);
+          dec_words[di] = bits;
           mbar_arrive(&dec_full[di]);
           kept_tiles += __popc(bits);
           if (p.decisions) {
@@ -439,67 +434,73 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[sb]);
+          if (tr) p.trace[kEvPDone * kTraceTiles + j] = clock64();
+          if (kTurns && j + 1 < ntiles) named_bar_arrive(turn_other, 256);
           continue;
         }
 
-        const bool mine = (bits >> gh) & 1u;
         float mx = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < TPR; ++q) {
-          const int hq_gate = (NH == 2) ? (q * CW) / 64 : 0;
-          if ((bits >> hq_gate) & 1u) mx = fmaxf(mx, pq[q]);
-        }
+        for (int h = 0; h < NH; ++h)
+          if ((bits >> h) & 1u) mx = fmaxf(mx, rm[h]);
         const float m_new = fmaxf(m_ref, mx);
+        const bool need = o_valid && m_new > m_ref + p.rescale_raw;
         float alpha = 1.f;
         if (!o_valid) {
           m_ref = m_new;
-        } else if (do_rescale && m_new > m_ref + p.rescale_raw) {
+        } else if (need) {
           alpha = ex2_approx((m_ref - m_new) * sl2);
           m_ref = m_new;
         }
-        if (mine) {
-          // P = exp2(s * scale*log2e - m * scale*log2e), bf16-packed over S
-          const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
-          const uint64_t sl2x2 = f2_pack(sl2, sl2);
-          const uint64_t negx2 = f2_pack(neg, neg);
-          uint64_t acc0 = 0, acc1 = 0;
-          uint32_t pk[CW / 2];
+
+        // P = exp2(s * scale*log2e - m * scale*log2e) for the kept gate tiles,
+        // bf16-packed over the S slot
+        const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
+        const uint64_t sl2x2 = f2_pack(sl2, sl2);
+        const uint64_t negx2 = f2_pack(neg, neg);
+        uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
-          for (int c = 0; c < CW; c += 4) {
-            const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2x2, negx2);
-            const uint64_t x1 =
-                ffma2(f2_pack(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), sl2x2, negx2);
-            const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
-            const float p2 = ex2_approx(f2_lo(x1)), p3 = ex2_approx(f2_hi(x1));
-            acc0 = fadd2(acc0, f2_pack(p0, p1));
-            acc1 = fadd2(acc1, f2_pack(p2, p3));
-            pk[c / 2] = pack_bf16x2(p0, p1);
-            pk[c / 2 + 1] = pack_bf16x2(p2, p3);
+        for (int h = 0; h < NH; ++h) {
+          if ((bits >> h) & 1u) {
+#pragma unroll
+            for (int cb = 0; cb < BN; cb += 32) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int c = 0; c < 32; c += 4) {
+                const int e = h * BN + cb + c;
+                const uint64_t x0 =
+                    ffma2(f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2, negx2);
+                const uint64_t x1 =
+                    ffma2(f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])), sl2x2, negx2);
+                const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
+                float p2, p3;
+                // offload part of the exponentials from the MUFU to the FMA pipe
+                if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
+                  const uint64_t e1 = exp2_poly_x2(x1);
+                  p2 = f2_lo(e1);
+                  p3 = f2_hi(e1);
+                } else {
+                  p2 = ex2_approx(f2_lo(x1));
+                  p3 = ex2_approx(f2_hi(x1));
+                }
+                acc0 = fadd2(acc0, f2_pack(p0, p1));
+                acc1 = fadd2(acc1, f2_pack(p2, p3));
+                pk[c / 2] = pack_bf16x2(p0, p1);
+                pk[c / 2 + 1] = pack_bf16x2(p2, p3);
+              }
+              tmem_st16(s_row + (h * BN + cb) / 2, pk);
+            }
           }
-          // P columns [cq*CW/2, (cq+1)*CW/2) of the slot
-          if constexpr (CW == 64) {
-            tmem_st32(s_row + cq * (CW / 2), pk);
-          } else {
-            tmem_st16(s_row + cq * (CW / 2), pk);
-          }
-          const uint64_t acc = fadd2(acc0, acc1);
-          l_part = l_part * alpha + (f2_lo(acc) + f2_hi(acc));
-        } else {
-          l_part = l_part * alpha;
         }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[sb]);
-        if (do_rescale) {
-          // rare: the running max grew by > 2^8; rescale this thread's O columns
-          // once every issued MMA (incl. PV_{j-1}) has landed
-          mbar_wait(o_quiet, n_rescale & 1);
-          ++n_rescale;
-          tc_fence_after();
+        const uint64_t acc = fadd2(acc0, acc1);
+        l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
+
+        if (__any_sync(0xffffffffu, need)) {
+          // Safe: this slot's QK commit certified every earlier PV into O_grp,
+          // and PV_j is only issued after p_full below.
           const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
-          for (int c = 0; c < DH; c += 32) {
+          for (int c = 0; c < D; c += 32) {
             uint32_t ov[32];
             tmem_ld32(o_tm + c, ov);
             tmem_wait_ld();
@@ -511,20 +512,23 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
             }
             tmem_st32(o_tm + c, ov);
           }
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(o_rescaled);
         }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        if (tr) p.trace[kEvPDone * kTraceTiles + j] = clock64();
+        if (kTurns && j + 1 < ntiles) named_bar_arrive(turn_other, 256);
         o_valid = true;
       }
     }
 
     if constexpr (CALIB) {
       // ---- order statistics of this row of tile maxima (calibration.py:116-153)
+      constexpr int NTHR = 128 * NG;
       const int A = ntiles * NH;
-      const int t = cq * 128 + r;  // 0..NTHR-1
-      named_bar_sync(1, NTHR);
+      const int t = grp * 128 + r;
+      named_bar_sync(3, NTHR);
       int* vals = cvals;
       if (p.c_maxima) {
         float* out = p.c_maxima + ((long long)hq * p.num_q_tiles + qi) * p.gate_cols;
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
               }
             }
           }
-          named_bar_sync(1, NTHR);
+          named_bar_sync(3, NTHR);
         }
       }
       if (t < p.c_num_levels) {
@@ -573,41 +577,67 @@ __global__ void __launch_bounds__((4 * TPR + 3) * 32, 1)
         if (tie) atomicAdd(&p.c_ties[t], 1ull);
       }
     } else {
-      // ---- epilogue: O / l -> bf16, lse = m*scale + ln(l)   (engine.py:178-182)
-      sts_f32(xch_l + (cq * 128 + r) * 4, l_part);
+      // ---- epilogue: merge the two groups' (m, l, O) and normalise
+      //      (engine.py:178-182: O = O~/l, lse = m*scale + ln l)
+      sts_f32(xch_fin + (grp * 128 + r) * 8, m_ref);
+      sts_f32(xch_fin + (grp * 128 + r) * 8 + 4, l_sum);
       mbar_wait(o_full, 0);
       tc_fence_after();
-      named_bar_sync(1, NTHR);
-      float l_sum = 0.f;
+      named_bar_sync(3, 128 * NG);
+      float mg[NG], lg[NG];
 #pragma unroll
-      for (int q = 0; q < TPR; ++q) l_sum += (q == cq) ? l_part : lds_f32(xch_l + (q * 128 + r) * 4);
-      const float inv_l = 1.f / l_sum;
-      bool bad = !(l_sum > 0.f);
+      for (int q = 0; q < NG; ++q) {
+        mg[q] = lds_f32(xch_fin + (q * 128 + r) * 8);
+        lg[q] = lds_f32(xch_fin + (q * 128 + r) * 8 + 4);
+      }
+      float m_all = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < NG; ++q)
+        if (lg[q] > 0.f) m_all = fmaxf(m_all, mg[q]);
+      float wgt[NG];
+      float l_all = 0.f;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        wgt[q] = lg[q] > 0.f ? ex2_approx((mg[q] - m_all) * sl2) : 0.f;
+        l_all += lg[q] * wgt[q];
+      }
+      const float inv_l = 1.f / l_all;
+      bool bad = !(l_all > 0.f);
+      constexpr int DH = D / NG;  // output columns written by this thread
       const int row = qi * 128 + r;
       __nv_bfloat16* orow =
-          p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + cq * DH;
+          p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + grp * DH;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {
-        uint32_t ov[32];
-        tmem_ld32(o_tm + c, ov);
-        tmem_wait_ld();
-        if (p.inject_fault && qi == 0 && r == 0 && cq == 0 && c == 0)
-          ov[0] = __float_as_uint(__uint_as_float(ov[0]) + l_sum);  // +1.0 on O[0][0]
+        float acc[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          if (lg[q] > 0.f) {  // an O slot nobody accumulated into holds garbage
+            uint32_t ov[32];
+            tmem_ld32(tmem + lane_off + q * D + grp * DH + c, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = fmaf(__uint_as_float(ov[e]), wgt[q], acc[e]);
+          }
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float a0 = __uint_as_float(ov[e]), a1 = __uint_as_float(ov[e + 1]);
+          float a0 = acc[e] * inv_l, a1 = acc[e + 1] * inv_l;
+          if (p.inject_fault && qi == 0 && r == 0 && grp == 0 && c == 0 && e == 0) a0 += 1.0f;  // O[0][0] += 1
           bad |= !isfinite(a0) || !isfinite(a1);
-          pk[e / 2] = pack_bf16x2(a0 * inv_l, a1 * inv_l);
+          pk[e / 2] = pack_bf16x2(a0, a1);
         }
         uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
         for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
       }
-      if (cq == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * p.scale + logf(l_sum);
+      if (grp == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_all * p.scale + logf(l_all);
       if (bad && p.status) atomicOr(p.status, 1);
-      if (warp == 0 && lane == 0 && p.counters) {
-        atomicAdd(&p.counters[0], (unsigned long long)ntiles * NH);
+      if (r == 0 && p.counters) {
+        if (grp == 0) atomicAdd(&p.counters[0], (unsigned long long)ntiles * NH);
         atomicAdd(&p.counters[1], kept_tiles);
       }
     }
