@@ -109,7 +109,7 @@ int bsfa_device_supported(void);
 
 int bsfa_fwd(const bsfa_fwd_args* args, void* stream);
 /* Debug: subsequent bsfa_fwd launches record per-tile clock64 timestamps of
-   CTA `cta` into dev_buf (int64 [6][4096]); NULL disables. */
+   CTA `cta` into dev_buf (int64 [8][4096]); NULL disables. */
 int bsfa_debug_trace(long long* dev_buf, int cta);
 int bsfa_calib_blockmax(const bsfa_calib_args* args, void* stream);
 int bsfa_calib_finalize(const double* finite_sum, const int32_t* finite_cnt, const int32_t* neg_cnt,

@@ -73,11 +73,11 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
-template <int D, int NH, bool CALIB>
+template <int D, int KT, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  using C = KCfg<D, NH, CALIB>;
-  auto kern = bsfa_kernel<D, NH, CALIB>;
+  using C = KCfg<D, KT, CALIB>;
+  auto kern = bsfa_kernel<D, KT, CALIB>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -92,16 +92,16 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 }
 
 template <bool CALIB>
-int dispatch(int d, int nh, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+int dispatch(int d, int kt, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& p, int grid, cudaStream_t st) {
-#define BSFA_CASE(D_, NH_) \
-  if (d == D_ && nh == NH_) return launch<D_, NH_, CALIB>(tq, tk, tv, p, grid, st);
-  BSFA_CASE(64, 1)
-  BSFA_CASE(64, 2)
-  BSFA_CASE(128, 1)
-  BSFA_CASE(128, 2)
+#define BSFA_CASE(D_, KT_) \
+  if (d == D_ && kt == KT_) return launch<D_, KT_, CALIB>(tq, tk, tv, p, grid, st);
+  BSFA_CASE(64, 64)
+  BSFA_CASE(64, 128)
+  BSFA_CASE(128, 64)
+  BSFA_CASE(128, 128)
 #undef BSFA_CASE
-  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d gate tiles per MMA tile=%d", d, nh);
+  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, kt);
 }
 
 int check_tiles(int b_m, int b_n) {
@@ -154,7 +154,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   CUtensorMap tq, tk, tv;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, 128, "k"))
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, a->b_n,
+                       "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))
@@ -169,7 +170,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.seq_len = n;
   p.valid_len = a->valid_len;
   p.num_q_tiles = n / 128;
-  p.num_kv_tiles = n / 128;
+  p.num_kv_tiles = n / a->b_n;  // key tiles of b_n keys
   p.gate_cols = n / a->b_n;
   p.causal = a->causal ? 1 : 0;
   p.gate_mode = a->gate_mode;
@@ -190,10 +191,9 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.counters = a->counters;
   p.status = a->status;
 
-  const int nh = 128 / a->b_n;
   const long long grid = (long long)a->batch * a->heads_q * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
-  return dispatch<false>(d, nh, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch<false>(d, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
@@ -205,8 +205,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
-  if (a->seq_len / a->b_n > KCfg<64, 2, true>::MAXA)
-    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, true>::MAXA);
+  if (a->seq_len / a->b_n > KCfg<64, 64, true>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 64, true>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
   if (a->seq_len / a->b_m > a->num_positions)
@@ -217,7 +217,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   const int d = a->head_dim, n = a->seq_len;
   CUtensorMap tq, tk;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, 1, a->q_stride_n, a->q_stride_h, 0, 128, "q")) return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, 128, "k")) return rc;
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, a->b_n, "k")) return rc;
 
   KernelParams p;
   memset(&p, 0, sizeof(p));
@@ -228,7 +228,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.seq_len = n;
   p.valid_len = n;
   p.num_q_tiles = n / 128;
-  p.num_kv_tiles = n / 128;
+  p.num_kv_tiles = n / a->b_n;
   p.gate_cols = n / a->b_n;
   p.causal = 1;
   p.scale = a->scale;
@@ -248,9 +248,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.c_ties = a->tie_counts;
   p.c_maxima = a->block_maxima;
 
-  const int nh = 128 / a->b_n;
   const int grid = a->heads_q * p.num_q_tiles;
-  return dispatch<true>(d, nh, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch<true>(d, a->b_n, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -1,7 +1,8 @@
 // BSFA forward (K1) and calibration block-max (K2) kernels for sm_100a.
 //
 // One CTA owns one query tile (128 rows of one q head, query block i) and
-// streams the reachable 128-key tiles of that head's kv head.  Warp roles:
+// streams the reachable key tiles (one gate tile of b_n keys each) of that
+// head's kv head.  Warp roles:
 //   warps 0..7   softmax, two groups of 4 warps.  Group g owns the key tiles
 //                j = g (mod 2) of this query tile: thread r of a group owns
 //                row r (TMEM lane r) over all 128 keys of the tile, keeps its
@@ -12,13 +13,14 @@
 //   warp 9       tcgen05 issuer (warp-convergent, one elected lane) + TMEM owner
 //   warp 10      TMA producer for V: fetches a V gate tile only when the
 //                gate kept it (decision ring from the softmax groups)
-// TMEM: O_0, O_1 (fp32, d columns each) and one S slot (fp32, 128 columns)
-// per group; P (bf16) is written over the slot and read by the PV MMA (A
-// operand from TMEM).  While one group runs its exponentials the tensor
-// cores run the other group's PV and next QK^T.
+// TMEM: O_0, O_1 (fp32, d columns each) and a ring of S slots (fp32, b_n
+// columns; 4 slots at b_n = 64, i.e. two per group); P (bf16) is written
+// over its slot and read by the PV MMA (A operand from TMEM).  QK^T of a
+// group's next tile is already in flight while the group works on the
+// current one, and the other group's PV runs under its exponentials.
 //
-// Per 128-key tile j (group g = j mod 2):
-//   QK:   S_g = Q K_j^T                   8 x tcgen05.mma 128x128x16 (SS)
+// Per key tile j of b_n = 64 or 128 keys (group g = j mod 2):
+//   QK:   S = Q K_j^T                     tcgen05.mma 128 x b_n x 16 (SS)
 //   gate: per gate tile, OR over rows of (rowmax * scale > T) == the
 //         reference's tile.s_max > T (gates.py:77-78, engine.py:30-38)
 //   skip: no V TMA, no exp, no PV MMA, no statistics update (engine.py:172-174)
@@ -38,19 +40,20 @@
 // exponentials run while the other group's PV/QK are on the tensor cores,
 // instead of both groups sharing the MUFUs and then both waiting.
 #ifndef BSFA_TURNS
-#define BSFA_TURNS 1
+#define BSFA_TURNS 0
 #endif
 
 namespace bsfa {
 
 enum : int { kGateThreshold = 0, kGateDense = 1, kGateFrontier = 2 };
+constexpr uint32_t kRescaleFlag = 0x80000000u;  // decision-word bit: rescale O_g before this tile's PV
 
 struct KernelParams {
   int batch, heads_q, heads_kv, group;
   int seq_len;       // padded sequence length (multiple of 128)
   int valid_len;     // unpadded length (non-causal key masking)
   int num_q_tiles;   // seq_len / 128
-  int num_kv_tiles;  // seq_len / 128
+  int num_kv_tiles;  // seq_len / b_n
   int gate_cols;     // seq_len / b_n
   int causal;
   int gate_mode;
@@ -82,21 +85,25 @@ struct KernelParams {
 
 // trace slots: trace[ev * kTraceTiles + j]
 constexpr int kTraceTiles = 4096;
-enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvIssued = 4, kEvSReadyG1 = 5 };
+enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvIssued = 4, kEvVReady = 5, kEvKReady = 6 };
 
-template <int D, int NH, bool CALIB>
+template <int D, int KT_, bool CALIB>
 struct KCfg {
-  static constexpr int KT = 128;             // keys per MMA tile
-  static constexpr int BN = KT / NH;         // gate tile width (reference b_n)
+  static constexpr int KT = KT_;             // keys per MMA tile == gate tile width (reference b_n)
   static constexpr int NCH = D / 64;         // 128-byte swizzle atoms along head_dim
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = KT * D * 2;
-  static constexpr int V_TILE = BN * D * 2;  // one gate tile of V
+  static constexpr int V_TILE = KT * D * 2;
   static constexpr int NG = 2;               // softmax groups (alternate key tiles)
-  static constexpr int NS = CALIB ? 4 : NG;  // S slots in TMEM (slot = tile mod NS)
-  static constexpr int KS = CALIB ? 4 : (D == 128 ? 2 : 3);  // K ring depth in smem
-  static constexpr int VS = CALIB ? 0 : (D == 128 ? 6 : 12) / (3 - NH);  // V gate-tile slots (96 KB ring)
-  static constexpr int DQ = 8;               // decision ring depth
+  // S slots in TMEM (slot = tile mod NS).  With 64-key tiles each group owns
+  // two slots, so QK^T of its next tile runs while it works on the current one.
+  static constexpr int NS_FIT = (512 - NG * D) / KT;
+  static constexpr int NS = CALIB ? 512 / KT / 2 : (NS_FIT < 4 ? NS_FIT : 4);
+  // K ring 96 KB (TMA latency from L2/HBM is 2-4k cycles under load: K must be
+  // requested several tiles ahead); V ring 80 KB.
+  static constexpr int KS = (D == 128 ? 98304 : 65536) / K_TILE;
+  static constexpr int VS = CALIB ? 0 : (D == 128 ? 81920 : 65536) / V_TILE;
+  static constexpr int DQ = 16;              // decision ring depth
   static constexpr int MAXA = 4096;          // calibration: max off-frontier gate tiles per row
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_TILE;
@@ -104,7 +111,7 @@ struct KCfg {
   static constexpr int OFF_CAL = OFF_V + VS * V_TILE;
   static constexpr int CAL_BYTES = CALIB ? MAXA * 4 : 0;
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 2 * NS + 2 * DQ + 1;
+  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 2 * NS + 2 * DQ + 1 + 2 * NG;
   static constexpr int OFF_XCH = OFF_BAR + NUM_BARS * 8;  // votes u32 [NG][2][4], final (m,l) f32 [NG][128][2]
   static constexpr int XCH_BYTES = NG * 2 * 4 * 4 + NG * 128 * 8;
   static constexpr int OFF_DEC = OFF_XCH + XCH_BYTES;
@@ -119,19 +126,21 @@ struct KCfg {
   static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static constexpr int VPROD_WARP = SOFTMAX_WARPS + 2;
   static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 3) * 32;
+  static_assert(KT == 64 || KT == 128, "64- or 128-key tiles");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(TMEM_NEED <= 512, "TMEM budget");
-  static_assert(CALIB || VS >= 2 * NH, "V ring must hold two tiles");
+  static_assert(NS >= 2, "at least one S slot per softmax group");
+  static_assert(CALIB || VS >= 2, "V ring must hold two tiles");
   static_assert(DQ >= NS && DQ >= KS, "decision ring depth");
 };
 
-template <int D, int NH, bool CALIB>
+template <int D, int KT_, bool CALIB>
 __global__ void __launch_bounds__(11 * 32, 1)
     bsfa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = KCfg<D, NH, CALIB>;
-  constexpr int KT = C::KT, BN = C::BN, KS = C::KS, VS = C::VS, NS = C::NS, DQ = C::DQ, NG = C::NG;
-  constexpr uint32_t HMASK = (1u << NH) - 1u;
+  using C = KCfg<D, KT_, CALIB>;
+  constexpr int KT = C::KT, KS = C::KS, VS = C::VS, NS = C::NS, DQ = C::DQ, NG = C::NG;
+  constexpr int TPQ = 128 / KT;  // key tiles per query-block width
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -150,6 +159,8 @@ __global__ void __launch_bounds__(11 * 32, 1)
   uint64_t* dec_full = p_full + NS;
   uint64_t* dec_empty = dec_full + DQ;
   uint64_t* o_full = dec_empty + DQ;
+  uint64_t* o_quiet = o_full + 1;        // [NG] MMA commit: all issued MMAs landed (O_g may be rescaled)
+  uint64_t* o_rescaled = o_quiet + NG;   // [NG] group g finished rescaling O_g
   volatile uint32_t* dec_words = reinterpret_cast<volatile uint32_t*>(smem + C::OFF_DEC);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
   const uint32_t xch_vote = smem_u32(smem + C::OFF_XCH);  // u32 [NG][2][4] per-warp gate votes
@@ -168,7 +179,10 @@ __global__ void __launch_bounds__(11 * 32, 1)
   const int b = bg / p.heads_kv;
   const int g = bg - b * p.heads_kv;
   const int hq = g * p.group + (rem - (rem / p.group) * p.group);
-  const int ntiles = CALIB ? qi : (p.causal ? qi + 1 : p.num_kv_tiles);
+  // reachable key tiles: causal -> through the frontier (key tiles overlapping
+  // the query rows, tiling.py:50-60); calibration -> the off-frontier prefix only
+  const int ntiles = CALIB ? qi * TPQ : (p.causal ? (qi + 1) * TPQ : p.num_kv_tiles);
+  const int fr_lo = qi * TPQ;  // first frontier tile
 
   // ---- setup
   if (warp == C::KPROD_WARP && lane == 0) {
@@ -190,6 +204,10 @@ __global__ void __launch_bounds__(11 * 32, 1)
       mbar_init(&dec_empty[i], 1);
     }
     mbar_init(o_full, 1);
+    for (int i = 0; i < NG; ++i) {
+      mbar_init(&o_quiet[i], 1);
+      mbar_init(&o_rescaled[i], 4);
+    }
     fence_mbarrier_init();
   }
   if constexpr (CALIB) {
@@ -234,21 +252,18 @@ __global__ void __launch_bounds__(11 * 32, 1)
         for (int j = 0; j < ntiles; ++j) {
           const int di = j % DQ;
           mbar_wait(&dec_full[di], (j / DQ) & 1);
-          const uint32_t bits = __shfl_sync(0xffffffffu, dec_words[di], 0) & HMASK;
+          const uint32_t keep = __shfl_sync(0xffffffffu, dec_words[di], 0);
           __syncwarp();
           mbar_arrive_w(&dec_empty[di]);
+          if (keep) {
+            const int slot = int(vcount % VS);
+            mbar_wait(&v_empty[slot], uint32_t((vcount / VS) & 1) ^ 1u);
+            mbar_arrive_expect_tx_w(&v_full[slot], C::V_TILE);
 #pragma unroll
-          for (int h = 0; h < NH; ++h) {
-            if ((bits >> h) & 1u) {
-              const int slot = int(vcount % VS);
-              mbar_wait(&v_empty[slot], uint32_t((vcount / VS) & 1) ^ 1u);
-              mbar_arrive_expect_tx_w(&v_full[slot], C::V_TILE);
-#pragma unroll
-              for (int c = 0; c < C::NCH; ++c)
-                tma_load_4d_w(sV + slot * C::V_TILE + c * BN * 128, &tm_v, &v_full[slot], c * 64, j * KT + h * BN,
-                              g, b, kEvictLast);
-              ++vcount;
-            }
+            for (int c = 0; c < C::NCH; ++c)
+              tma_load_4d_w(sV + slot * C::V_TILE + c * KT * 128, &tm_v, &v_full[slot], c * 64, j * KT, g, b,
+                            kEvictLast);
+            ++vcount;
           }
         }
         if (lane == 0 && p.counters) atomicAdd(&p.counters[2], vcount);
@@ -263,15 +278,17 @@ __global__ void __launch_bounds__(11 * 32, 1)
       // descriptor templates; per-MMA offsets only touch the 14-bit start-address field
       const uint64_t dq0 = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dk0 = make_sdesc_sw128(smem_u32(sK), 16, 1024);
-      const uint64_t dv0 = make_sdesc_sw128(smem_u32(sV), BN * 128, 1024);
+      const uint64_t dv0 = make_sdesc_sw128(smem_u32(sV), KT * 128, 1024);
       mbar_wait(bar_q, 0);
 
       auto issue_qk = [&](int t) {
         const int st = t % KS;
         mbar_wait(&k_full[st], (t / KS) & 1);
+        if (p.trace && (int)blockIdx.x == p.trace_cta && lane == 0 && t < kTraceTiles)
+          p.trace[kEvKReady * kTraceTiles + t] = clock64();
         tc_fence_after();
         const uint32_t d_tmem = tmem + C::S_COL + (t % NS) * KT;
-        umma_qk_tile_w<D>(d_tmem, dq0, dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
+        umma_qk_tile_w<D, KT>(d_tmem, dq0, dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
         umma_commit_w(&s_full[t % NS]);
         umma_commit_w(&k_empty[st]);
       };
@@ -281,6 +298,7 @@ __global__ void __launch_bounds__(11 * 32, 1)
 
       unsigned long long vcount = 0;
       uint32_t o_started = 0;  // bit g: O_g holds a partial sum
+      uint32_t n_rescale = 0;  // bit g: parity of group g's rescale hand-offs
       for (int j = 0; j < ntiles; ++j) {
         const int sb = j % NS;
         mbar_wait(&p_full[sb], (j / NS) & 1);
@@ -288,24 +306,30 @@ __global__ void __launch_bounds__(11 * 32, 1)
         if (tr) p.trace[kEvPSeen * kTraceTiles + j] = clock64();
         if constexpr (!CALIB) {
           const int og = j % NG;
-          const uint32_t bits = __shfl_sync(0xffffffffu, dec_words[j % DQ], 0) & HMASK;
+          const uint32_t word = __shfl_sync(0xffffffffu, dec_words[j % DQ], 0);
+          const uint32_t keep = word & 1u;
           const uint32_t p_tmem = tmem + C::S_COL + sb * KT;
+          if (word & kRescaleFlag) {
+            // group og rescales O_og in TMEM: let every issued MMA land first,
+            // and hold PV_j until the rescale is done (rare: max grew by > 2^8)
+            umma_commit_w(&o_quiet[og]);
+            mbar_wait(&o_rescaled[og], (n_rescale >> og) & 1);
+            n_rescale ^= 1u << og;
+            tc_fence_after();
+          }
+          if (keep) {
+            const int slot = int(vcount % VS);
+            mbar_wait(&v_full[slot], uint32_t((vcount / VS) & 1));
+            if (tr) p.trace[kEvVReady * kTraceTiles + j] = clock64();
+            ++vcount;
+            tc_fence_after();
+            const uint64_t dv = dv0 + uint64_t((slot * C::V_TILE) >> 4);
 #pragma unroll
-          for (int h = 0; h < NH; ++h) {
-            if ((bits >> h) & 1u) {
-              const int slot = int(vcount % VS);
-              mbar_wait(&v_full[slot], uint32_t((vcount / VS) & 1));
-              ++vcount;
-              tc_fence_after();
-              const uint64_t dv = dv0 + uint64_t((slot * C::V_TILE) >> 4);
-#pragma unroll
-              for (int q = 0; q < BN / 64; ++q) {  // 64 keys per batch (1 for b_n=64, 2 for b_n=128)
-                umma_pv64_w(tmem + og * D, p_tmem + (h * BN + q * 64) / 2, dv + uint64_t(q * 512), IDESC_PV,
-                            (o_started >> og) & 1u);
-                o_started |= 1u << og;
-              }
-              umma_commit_w(&v_empty[slot]);
+            for (int q = 0; q < KT / 64; ++q) {  // 64 keys per batch
+              umma_pv64_w(tmem + og * D, p_tmem + q * 32, dv + uint64_t(q * 512), IDESC_PV, (o_started >> og) & 1u);
+              o_started |= 1u << og;
             }
+            umma_commit_w(&v_empty[slot]);
           }
           if (j == ntiles - 1) umma_commit_w(o_full);
         } else {
@@ -341,6 +365,7 @@ __global__ void __launch_bounds__(11 * 32, 1)
     float m_ref = -INFINITY;  // raw (unscaled) reference max of this row over this group's kept tiles
     float l_sum = 0.f;        // row sum relative to m_ref
     bool o_valid = false;     // group-uniform: O_g holds data
+    uint32_t n_rescale = 0;
     unsigned long long kept_tiles = 0;
 
     for (int j = grp; j < ntiles; j += NG) {
@@ -357,12 +382,13 @@ __global__ void __launch_bounds__(11 * 32, 1)
       for (int c = 0; c < KT; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
 
-      const bool frontier = (j == qi);
+      const bool frontier = (j >= fr_lo) && (j < fr_lo + TPQ);
       if (!CALIB) {
         if (frontier && p.causal) {
+          const int off = (j - fr_lo) * KT;  // key - row offset inside the query block
 #pragma unroll
           for (int c = 0; c < KT; ++c)
-            if (c > r) sv[c] = __float_as_uint(-INFINITY);
+            if (off + c > r) sv[c] = __float_as_uint(-INFINITY);
         }
         if (!p.causal && (j + 1) * KT > p.valid_len) {
 #pragma unroll
@@ -370,30 +396,28 @@ __global__ void __launch_bounds__(11 * 32, 1)
             if (j * KT + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
         }
       }
-      float rm[NH];  // row max per gate tile
+      float rm;  // row max of the tile (one gate tile)
+      {
+        float m0 = fmaxf(__uint_as_float(sv[0]), __uint_as_float(sv[1]));
+        float m1 = fmaxf(__uint_as_float(sv[2]), __uint_as_float(sv[3]));
+        float m2 = fmaxf(__uint_as_float(sv[4]), __uint_as_float(sv[5]));
+        float m3 = fmaxf(__uint_as_float(sv[6]), __uint_as_float(sv[7]));
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        float m0 = fmaxf(__uint_as_float(sv[h * BN]), __uint_as_float(sv[h * BN + 1]));
-        float m1 = fmaxf(__uint_as_float(sv[h * BN + 2]), __uint_as_float(sv[h * BN + 3]));
-        float m2 = fmaxf(__uint_as_float(sv[h * BN + 4]), __uint_as_float(sv[h * BN + 5]));
-        float m3 = fmaxf(__uint_as_float(sv[h * BN + 6]), __uint_as_float(sv[h * BN + 7]));
-#pragma unroll
-        for (int c = 8; c < BN; c += 8) {
-          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[h * BN + c]), __uint_as_float(sv[h * BN + c + 1])));
-          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[h * BN + c + 2]), __uint_as_float(sv[h * BN + c + 3])));
-          m2 = fmaxf(m2, fmaxf(__uint_as_float(sv[h * BN + c + 4]), __uint_as_float(sv[h * BN + c + 5])));
-          m3 = fmaxf(m3, fmaxf(__uint_as_float(sv[h * BN + c + 6]), __uint_as_float(sv[h * BN + c + 7])));
+        for (int c = 8; c < KT; c += 8) {
+          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])));
+          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])));
+          m2 = fmaxf(m2, fmaxf(__uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5])));
+          m3 = fmaxf(m3, fmaxf(__uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7])));
         }
-        rm[h] = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        rm = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
       }
 
       if constexpr (CALIB) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          float m = rm[h];
+        {
+          float m = rm;
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-          if (lane == 0) atomicMax(&cvals[j * NH + h], float_to_ordered(m * p.scale));
+          if (lane == 0) atomicMax(&cvals[j], float_to_ordered(m * p.scale));
         }
         tc_fence_before();
         __syncwarp();
@@ -401,33 +425,36 @@ __global__ void __launch_bounds__(11 * 32, 1)
         continue;
       } else {
         // ---- gate: OR over the group's 128 rows of (rowmax * scale > T)
+        // one group-wide exchange per tile: gate vote (bit 0) and a rescale
+        // request (bit 1: this row's max outgrows the running reference)
+        const bool gvote = p.gate_mode == kGateThreshold && rm * p.scale > T;
+        const bool rreq = o_valid && rm > m_ref + p.rescale_raw;
+        const uint32_t wv = (__ballot_sync(0xffffffffu, gvote) != 0u ? 1u : 0u) |
+                            (__ballot_sync(0xffffffffu, rreq) != 0u ? 2u : 0u);
+        const uint32_t par = use & 1;
+        if (lane == 0) sts_u32(vote_base + (par * 4 + wq) * 4, wv);
+        named_bar_sync(1 + grp, 128);
+        const uint4 v4 = lds_u128(vote_base + par * 4 * 4);
+        const uint32_t vw = v4.x | v4.y | v4.z | v4.w;
         uint32_t bits;
         if (frontier || p.gate_mode == kGateDense) {
-          bits = HMASK;
+          bits = 1u;
         } else if (p.gate_mode == kGateFrontier) {
           bits = 0;
         } else {
-          uint32_t wv = 0;
-#pragma unroll
-          for (int h = 0; h < NH; ++h) wv |= (__ballot_sync(0xffffffffu, rm[h] * p.scale > T) != 0u ? 1u : 0u) << h;
-          const uint32_t par = use & 1;
-          if (lane == 0) sts_u32(vote_base + (par * 4 + wq) * 4, wv);
-          named_bar_sync(1 + grp, 128);
-          const uint4 v4 = lds_u128(vote_base + par * 4 * 4);
-          bits = (v4.x | v4.y | v4.z | v4.w) & HMASK;
+          bits = vw & 1u;
         }
+        const bool do_rescale = bits && (vw & 2u);
         if (tr) p.trace[kEvVoted * kTraceTiles + j] = clock64();
         if (r == 0) {
           const int di = j % DQ;
           mbar_wait(&dec_empty[di], ((j / DQ) & 1) ^ 1);
-          dec_words[di] = bits;
+          dec_words[di] = bits | (do_rescale ? kRescaleFlag : 0u);
           mbar_arrive(&dec_full[di]);
-          kept_tiles += __popc(bits);
+          kept_tiles += bits;
           if (p.decisions) {
             int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi) * p.gate_cols;
-#pragma unroll
-            for (int h = 0; h < NH; ++h)
-              drow[j * NH + h] = frontier ? int8_t(2) : (((bits >> h) & 1u) ? int8_t(3) : int8_t(1));
+            drow[j] = frontier ? int8_t(2) : (bits ? int8_t(3) : int8_t(1));
           }
         }
         if (bits == 0) {
@@ -439,65 +466,62 @@ __global__ void __launch_bounds__(11 * 32, 1)
           continue;
         }
 
-        float mx = -INFINITY;
-#pragma unroll
-        for (int h = 0; h < NH; ++h)
-          if ((bits >> h) & 1u) mx = fmaxf(mx, rm[h]);
-        const float m_new = fmaxf(m_ref, mx);
-        const bool need = o_valid && m_new > m_ref + p.rescale_raw;
+        const float m_new = fmaxf(m_ref, rm);
         float alpha = 1.f;
         if (!o_valid) {
           m_ref = m_new;
-        } else if (need) {
+        } else if (do_rescale && m_new > m_ref + p.rescale_raw) {
           alpha = ex2_approx((m_ref - m_new) * sl2);
           m_ref = m_new;
         }
 
-        // P = exp2(s * scale*log2e - m * scale*log2e) for the kept gate tiles,
-        // bf16-packed over the S slot
+        // P = exp2(s * scale*log2e - m * scale*log2e), bf16-packed over the S slot
         const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
         const uint64_t sl2x2 = f2_pack(sl2, sl2);
         const uint64_t negx2 = f2_pack(neg, neg);
         uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          if ((bits >> h) & 1u) {
+        for (int cb = 0; cb < KT; cb += 32) {
+          uint32_t pk[16];
 #pragma unroll
-            for (int cb = 0; cb < BN; cb += 32) {
-              uint32_t pk[16];
-#pragma unroll
-              for (int c = 0; c < 32; c += 4) {
-                const int e = h * BN + cb + c;
-                const uint64_t x0 =
-                    ffma2(f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2, negx2);
-                const uint64_t x1 =
-                    ffma2(f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])), sl2x2, negx2);
-                const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
-                float p2, p3;
-                // offload part of the exponentials from the MUFU to the FMA pipe
-                if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
-                  const uint64_t e1 = exp2_poly_x2(x1);
-                  p2 = f2_lo(e1);
-                  p3 = f2_hi(e1);
-                } else {
-                  p2 = ex2_approx(f2_lo(x1));
-                  p3 = ex2_approx(f2_hi(x1));
-                }
-                acc0 = fadd2(acc0, f2_pack(p0, p1));
-                acc1 = fadd2(acc1, f2_pack(p2, p3));
-                pk[c / 2] = pack_bf16x2(p0, p1);
-                pk[c / 2 + 1] = pack_bf16x2(p2, p3);
-              }
-              tmem_st16(s_row + (h * BN + cb) / 2, pk);
+          for (int c = 0; c < 32; c += 4) {
+            const int e = cb + c;
+            const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2, negx2);
+            const uint64_t x1 =
+                ffma2(f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])), sl2x2, negx2);
+            const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
+            float p2, p3;
+            // offload part of the exponentials from the MUFU to the FMA pipe
+            if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
+              const uint64_t e1 = exp2_poly_x2(x1);
+              p2 = f2_lo(e1);
+              p3 = f2_hi(e1);
+            } else {
+              p2 = ex2_approx(f2_lo(x1));
+              p3 = ex2_approx(f2_hi(x1));
             }
+            acc0 = fadd2(acc0, f2_pack(p0, p1));
+            acc1 = fadd2(acc1, f2_pack(p2, p3));
+            pk[c / 2] = pack_bf16x2(p0, p1);
+            pk[c / 2 + 1] = pack_bf16x2(p2, p3);
           }
+          tmem_st16(s_row + cb / 2, pk);
         }
         const uint64_t acc = fadd2(acc0, acc1);
         l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
 
-        if (__any_sync(0xffffffffu, need)) {
-          // Safe: this slot's QK commit certified every earlier PV into O_grp,
-          // and PV_j is only issued after p_full below.
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        if (tr) p.trace[kEvPDone * kTraceTiles + j] = clock64();
+        if (kTurns && j + 1 < ntiles) named_bar_arrive(turn_other, 256);
+        if (do_rescale) {
+          // hand-off with the MMA warp: wait until every issued MMA (incl. the
+          // group's previous PV) has landed, rescale O_grp, release PV_j
+          mbar_wait(&o_quiet[grp], n_rescale & 1);
+          ++n_rescale;
+          tc_fence_after();
           const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < D; c += 32) {
@@ -512,13 +536,11 @@ __global__ void __launch_bounds__(11 * 32, 1)
             }
             tmem_st32(o_tm + c, ov);
           }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_rescaled[grp]);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[sb]);
-        if (tr) p.trace[kEvPDone * kTraceTiles + j] = clock64();
-        if (kTurns && j + 1 < ntiles) named_bar_arrive(turn_other, 256);
         o_valid = true;
       }
     }
@@ -526,7 +548,7 @@ __global__ void __launch_bounds__(11 * 32, 1)
     if constexpr (CALIB) {
       // ---- order statistics of this row of tile maxima (calibration.py:116-153)
       constexpr int NTHR = 128 * NG;
-      const int A = ntiles * NH;
+      const int A = ntiles;
       const int t = grp * 128 + r;
       named_bar_sync(3, NTHR);
       int* vals = cvals;
@@ -637,7 +659,7 @@ __global__ void __launch_bounds__(11 * 32, 1)
       if (grp == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_all * p.scale + logf(l_all);
       if (bad && p.status) atomicOr(p.status, 1);
       if (r == 0 && p.counters) {
-        if (grp == 0) atomicAdd(&p.counters[0], (unsigned long long)ntiles * NH);
+        if (grp == 0) atomicAdd(&p.counters[0], (unsigned long long)ntiles);
         atomicAdd(&p.counters[1], kept_tiles);
       }
     }
