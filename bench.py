@@ -345,7 +345,7 @@ def main():
     torch.cuda.synchronize()
     clocks = clk.summary()
     cnt = plan.counters.cpu().numpy()
-    reach, kept, vload = int(cnt[0]), int(cnt[1]), int(cnt[2])
+    reach, kept, vload, vunits = int(cnt[0]), int(cnt[1]), int(cnt[2]), int(cnt[3])
     f_exec = costs.executed_flops(reach, kept, tiles, d)
     f_dense = costs.dense_flops(reach, tiles, d)
     ms_rank = total_ms / args.steps
@@ -412,7 +412,8 @@ def main():
                        "parallelism": f"kv-group/batch sharding x{world}, no collective",
                        "l2": "inputs (Q/K/V 384 MiB at 32K) exceed the 126 MB L2; no explicit flush",
                        "thresholds": "calibrated on a separate synthetic sample (seed 1000)"},
-            "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / reach,
+            "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / vunits,
+            "v_tile_fetches": {"loaded": vload, "loadable": vunits, "note": "one fetch per (CTA, gate tile) serves both q heads of the CTA"},
             "effective_dense_tflops": sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12 if world == 1
             else None,
             **dense, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BSFA_ABI_VERSION 1
+#define BSFA_ABI_VERSION 2
 
 /* error codes */
 #define BSFA_OK 0
@@ -49,7 +49,9 @@ extern "C" {
 /* counters written by bsfa_fwd (accumulated with atomics, caller zeroes) */
 #define BSFA_CNT_REACHABLE 0 /* reachable gate tiles (frontier included)        */
 #define BSFA_CNT_KEPT 1      /* processed gate tiles (frontier + kept)          */
-#define BSFA_CNT_VLOADS 2    /* V gate tiles fetched by TMA                     */
+#define BSFA_CNT_VLOADS 2    /* V gate tiles fetched by TMA (one fetch serves    */
+                             /* every query tile of a CTA that kept the tile)  */
+#define BSFA_CNT_VUNITS 3    /* V gate tiles a CTA could have fetched           */
 
 typedef struct bsfa_fwd_args {
   /* inputs: bf16 [batch][heads][seq][head_dim], arbitrary element strides with
@@ -65,7 +67,7 @@ typedef struct bsfa_fwd_args {
   int64_t o_stride_b, o_stride_h, o_stride_n;
   float* lse;        /* fp32 [batch][heads_q][seq_len], natural log, scaled-score units */
   int8_t* decisions; /* optional int8 [batch][heads_q][seq_len/b_m][seq_len/b_n]; caller zeroes */
-  unsigned long long* counters; /* optional [3], see BSFA_CNT_* */
+  unsigned long long* counters; /* optional [4], see BSFA_CNT_* */
   int* status; /* optional; bit 0 set if any row has a non-finite accumulator or l <= 0 */
   /* gate */
   const float* thresholds; /* fp32 [heads_q][thr_positions] (one level, one layer) */
@@ -108,8 +110,10 @@ const char* bsfa_last_error(void);
 int bsfa_device_supported(void);
 
 int bsfa_fwd(const bsfa_fwd_args* args, void* stream);
-/* Debug: subsequent bsfa_fwd launches record per-tile clock64 timestamps of
-   CTA `cta` into dev_buf (int64 [8][4096]); NULL disables. */
+/* Debug: in a library built with -DBSFA_TRACE=1, subsequent bsfa_fwd launches
+   record per-step clock64 timestamps of CTA `cta` into dev_buf
+   (int64 [6 events][2 query tiles][2048 steps]); NULL disables.  The
+   production build ignores the buffer. */
 int bsfa_debug_trace(long long* dev_buf, int cta);
 int bsfa_calib_blockmax(const bsfa_calib_args* args, void* stream);
 int bsfa_calib_finalize(const double* finite_sum, const int32_t* finite_cnt, const int32_t* neg_cnt,

@@ -16,7 +16,7 @@ from .errors import BsfaError
 LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 BSFA_OK = 0
 BSFA_ERR_INVALID = -1

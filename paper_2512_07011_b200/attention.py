@@ -46,7 +46,7 @@ class AttentionResult:
     o: torch.Tensor                  # [B, Hq, N, d] bf16
     lse: torch.Tensor                # [B, Hq, N] fp32
     decisions: torch.Tensor | None   # [B, Hq, M_q, M_kv] int8 (padded grid) or None
-    counters: torch.Tensor           # int64 [3]: reachable, kept, V tiles loaded
+    counters: torch.Tensor           # int64 [4]: reachable, kept, V tiles loaded, V tiles loadable
     status: torch.Tensor             # int32 [1]; non-zero = numeric failure
 
 
@@ -157,7 +157,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         lse = torch.empty((bsz, hq, n_pad), dtype=torch.float32, device=dev)
         m_q, m_kv = n_pad // tiles.b_m, n_pad // tiles.b_n
         dec = torch.zeros((bsz, hq, m_q, m_kv), dtype=torch.int8, device=dev) if return_trace else None
-        counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        counters = torch.zeros(4, dtype=torch.int64, device=dev)
         status = torch.zeros(1, dtype=torch.int32, device=dev)
 
         a = _lib.FwdArgs()
@@ -273,7 +273,7 @@ class BsfaPlan:
         m_q, m_kv = self.n_pad // tiles.b_m, self.n_pad // tiles.b_n
         self.decisions = (torch.zeros((batch, heads_q, m_q, m_kv), dtype=torch.int8, device=dev)
                           if return_trace else None)
-        self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         a = _lib.FwdArgs()
         a.o = self.o.data_ptr()

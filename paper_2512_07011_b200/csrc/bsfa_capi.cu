@@ -73,11 +73,11 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
-template <int D, int KT, bool CALIB>
+template <int D, int GT, int NQ, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  using C = KCfg<D, KT, CALIB>;
-  auto kern = bsfa_kernel<D, KT, CALIB>;
+  using C = KCfg<D, GT, NQ, CALIB>;
+  auto kern = bsfa_kernel<D, GT, NQ, CALIB>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -91,18 +91,26 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
   return BSFA_OK;
 }
 
+// NQ = 2 query tiles (two q heads of one GQA group) per CTA when the group
+// size is even, else 1.
 template <bool CALIB>
-int dispatch(int d, int kt, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+int dispatch(int d, int b_n, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& p, int grid, cudaStream_t st) {
-#define BSFA_CASE(D_, KT_) \
-  if (d == D_ && kt == KT_) return launch<D_, KT_, CALIB>(tq, tk, tv, p, grid, st);
-  BSFA_CASE(64, 64)
-  BSFA_CASE(64, 128)
-  BSFA_CASE(128, 64)
-  BSFA_CASE(128, 128)
+#define BSFA_CASE(D_, BN_, NQ_) \
+  if (d == D_ && b_n == BN_ && nq == NQ_) return launch<D_, 128 / BN_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
+  BSFA_CASE(64, 64, 1)
+  BSFA_CASE(64, 64, 2)
+  BSFA_CASE(64, 128, 1)
+  BSFA_CASE(64, 128, 2)
+  BSFA_CASE(128, 64, 1)
+  BSFA_CASE(128, 64, 2)
+  BSFA_CASE(128, 128, 1)
+  BSFA_CASE(128, 128, 2)
 #undef BSFA_CASE
-  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, kt);
+  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
 }
+
+int tiles_per_cta(int group) { return group % 2 == 0 ? 2 : 1; }
 
 int check_tiles(int b_m, int b_n) {
   if (b_m != 128 || (b_n != 64 && b_n != 128))
@@ -154,7 +162,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   CUtensorMap tq, tk, tv;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, a->b_n,
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, 128,
                        "k"))
     return rc;
   if (int rc =
@@ -170,7 +178,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.seq_len = n;
   p.valid_len = a->valid_len;
   p.num_q_tiles = n / 128;
-  p.num_kv_tiles = n / a->b_n;  // key tiles of b_n keys
+  p.num_steps = n / 128;  // 128-key MMA steps
   p.gate_cols = n / a->b_n;
   p.causal = a->causal ? 1 : 0;
   p.gate_mode = a->gate_mode;
@@ -191,9 +199,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.counters = a->counters;
   p.status = a->status;
 
-  const long long grid = (long long)a->batch * a->heads_q * p.num_q_tiles;
+  const int nq = tiles_per_cta(p.group);
+  const long long grid = (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
-  return dispatch<false>(d, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch<false>(d, a->b_n, nq, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
@@ -205,8 +214,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
-  if (a->seq_len / a->b_n > KCfg<64, 64, true>::MAXA)
-    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 64, true>::MAXA);
+  if (a->seq_len / a->b_n > KCfg<64, 2, 1, true>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, 1, true>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
   if (a->seq_len / a->b_m > a->num_positions)
@@ -217,7 +226,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   const int d = a->head_dim, n = a->seq_len;
   CUtensorMap tq, tk;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, 1, a->q_stride_n, a->q_stride_h, 0, 128, "q")) return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, a->b_n, "k")) return rc;
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, 128, "k")) return rc;
 
   KernelParams p;
   memset(&p, 0, sizeof(p));
@@ -228,7 +237,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.seq_len = n;
   p.valid_len = n;
   p.num_q_tiles = n / 128;
-  p.num_kv_tiles = n / a->b_n;
+  p.num_steps = n / 128;
   p.gate_cols = n / a->b_n;
   p.causal = 1;
   p.scale = a->scale;
@@ -248,8 +257,9 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.c_ties = a->tie_counts;
   p.c_maxima = a->block_maxima;
 
-  const int grid = a->heads_q * p.num_q_tiles;
-  return dispatch<true>(d, a->b_n, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+  const int nq = tiles_per_cta(p.group);
+  const int grid = (a->heads_q / nq) * p.num_q_tiles;
+  return dispatch<true>(d, a->b_n, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

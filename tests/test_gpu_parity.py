@@ -289,8 +289,12 @@ def test_determinism_and_counters(bsfa):
     dec = r1.decisions.cpu().numpy()
     c = r1.counters.cpu().numpy()
     assert c[0] == np.count_nonzero(dec) and c[1] == np.count_nonzero(dec >= 2)
-    # one V gate-tile fetch per processed (frontier or kept) tile, none for skipped ones
-    assert c[2] == np.count_nonzero(dec >= 2)
+    # a CTA owns two q heads of a GQA group (h, h+1) and fetches a V gate
+    # tile once if either head processes (frontier or kept) it, never if both skip
+    kept = dec >= 2
+    assert c[2] == np.count_nonzero(kept[:, 0::2] | kept[:, 1::2])
+    assert c[3] == np.count_nonzero(dec[:, 0::2])
+    assert c[2] < c[3]
     assert 0 < c[1] < c[0]
 
 

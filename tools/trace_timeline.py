@@ -1,7 +1,9 @@
-"""Per-tile timeline of one CTA (debug trace hook) for the L32K workload.
+"""Per-step timeline of one CTA (debug trace hook) for the L32K workload.
 
-Runs the BSFA and dense forward with bsfa_debug_trace enabled on CTA 0
-(query block 255, the longest) and prints median intervals (SM cycles).
+Needs the trace build:  nvcc ... -DBSFA_TRACE=1 -o paper_2512_07011_b200/_lib/variants/libbsfa_b200_trace.so
+and BSFA_LIB_PATH pointing at it.  Runs the BSFA and dense forward with
+bsfa_debug_trace on one CTA and prints median intervals (SM cycles) per
+query tile s of the CTA.
 """
 import ctypes
 import json
@@ -15,7 +17,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
-EV = ["SReady", "Voted", "PDone", "PSeen", "Issued"]
+EV = ["SReady", "Voted", "PDone", "PSeen", "VReady", "Issued"]
+STEPS = 2048
 
 
 def run(mode, seq=32768, cta=0):
@@ -33,7 +36,7 @@ def run(mode, seq=32768, cta=0):
         plan = bsfa.BsfaPlan(1, 32, 8, seq, 128, thresholds=thr, k_level=kl)
     else:
         plan = bsfa.BsfaPlan(1, 32, 8, seq, 128)
-    buf = torch.zeros((8, 4096), dtype=torch.int64, device=dev)
+    buf = torch.zeros((16, STEPS), dtype=torch.int64, device=dev)
     lib = _lib.load_library()
     plan.run(q, k, v)
     lib.bsfa_debug_trace(ctypes.c_void_p(buf.data_ptr()), cta)
@@ -41,33 +44,29 @@ def run(mode, seq=32768, cta=0):
     torch.cuda.synchronize()
     lib.bsfa_debug_trace(None, -1)
     t = buf.cpu().numpy().astype(np.int64)
-    per_bg = (seq // 128) * 4
-    qi = seq // 128 - 1 - (cta % per_bg) // 4
-    n = (qi + 1) * 2
-    sr, vo, pd, ps, iss, vr, kr = (t[i, :n] for i in range(7))
-    out = {}
-    out["softmax_C"] = np.median(pd - sr)
-    out["vote_part"] = np.median(vo - sr)
-    out["mma_lag_after_pdone"] = np.median(ps - pd)
-    out["mma_issue"] = np.median(iss - ps)
-    kept = vr > 0
-    out["v_wait_after_pseen"] = float(np.median((vr - ps)[kept])) if kept.any() else -1
-    out["v_ready_minus_voted"] = float(np.median((vr - vo)[kept])) if kept.any() else -1
-    out["k_ready(j+NS)_minus_pseen(j)"] = float(np.median(kr[4:] - ps[:-4]))
-    out["kept_frac"] = float(kept.mean())
-    out["chain_issue_to_sready_j+2"] = np.median(sr[2:] - iss[:-2])
-    out["per_tile_pdone_step"] = np.median(np.diff(pd))
-    out["per_tile_pseen_step"] = np.median(np.diff(ps))
-    out["total_cycles"] = int(pd[n - 1] - sr[0])
-    out["cycles_per_tile"] = out["total_cycles"] / n
-    print(mode, "cta", cta, "tiles", n, json.dumps({k: round(float(v), 1) for k, v in out.items()}))
-    # first 12 tiles raw (relative)
-    base = sr[0]
-    for j in range(0, 12):
-        print(f"  j={j:3d} S={sr[j]-base:8d} V={vo[j]-base:8d} P={pd[j]-base:8d} seen={ps[j]-base:8d} "
-              f"vrdy={(vr[j]-base) if vr[j] else -1:8d} krdy={kr[j]-base:8d} iss={iss[j]-base:8d}")
+    m_q = seq // 128
+    per_bg = m_q * 2
+    qi = m_q - 1 - (cta % per_bg) // 2
+    n = qi + 1
+    ev = {name: [t[e * 2 + s, :n] for s in range(2)] for e, name in enumerate(EV)}
+    base = ev["SReady"][0][0]
+    out = {"steps": n}
+    for s in range(2):
+        sr, vo, pd, ps, vr, iss = (ev[x][s] for x in EV)
+        out[f"s{s}_softmax(S->Pdone)"] = float(np.median(pd - sr))
+        out[f"s{s}_vote(S->Voted)"] = float(np.median(vo - sr))
+        out[f"s{s}_mma_lag(Pdone->Pseen)"] = float(np.median(ps - pd))
+        out[f"s{s}_mma_issue(Pseen->Issued)"] = float(np.median(iss - ps))
+        out[f"s{s}_S_wait(Issued_j->SReady_j+1)"] = float(np.median(sr[1:] - iss[:-1]))
+        out[f"s{s}_step"] = float(np.median(np.diff(pd)))
+    out["cycles_per_step"] = float((ev["PDone"][1][n - 1] - base) / n)
+    print(mode, "cta", cta, "qblock", qi, json.dumps({k: round(v, 1) for k, v in out.items()}))
+    for j in list(range(0, 6)) + list(range(n // 2, n // 2 + 4)):
+        row = " ".join(f"{x}{s}={int(ev[x][s][j] - base) if ev[x][s][j] else -1:8d}" for s in range(2) for x in EV)
+        print(f"  j={j:4d} {row}")
 
 
-for cta in (0, 2560):
-    for m in ("bsfa", "dense"):
-        run(m, cta=cta)
+if __name__ == "__main__":
+    for cta in (0, 1280):
+        for m in ("bsfa", "dense"):
+            run(m, cta=cta)
