@@ -92,7 +92,7 @@ struct KernelParams {
 
 // trace slots: trace[(ev * 2 + s) * kTraceSteps + j]
 constexpr int kTraceSteps = 2048;
-enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvVReady = 4, kEvIssued = 5 };
+enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvVReady = 4, kEvIssued = 5, kEvLdDone = 6, kEvExpDone = 7 };
 
 template <int D, int GT, int NQ, bool CALIB>
 struct KCfg {
@@ -111,9 +111,11 @@ struct KCfg {
   static constexpr int OFF_CAL = OFF_V + VS * V_UNIT;
   static constexpr int CAL_BYTES = CALIB ? NQ * MAXA * 4 : 0;
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 3 * NQ + 2 * NQ * DQ;
-  static constexpr int OFF_VOTE = (OFF_BAR + NUM_BARS * 8 + 15) / 16 * 16;  // u32 [NQ][2][4] per-warp gate votes (16-B aligned: read as v4)
-  static constexpr int OFF_DEC = OFF_VOTE + NQ * 8 * 4;     // u32 [NQ][DQ] decision ring (V producer)
+  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 4 * NQ + 2 * NQ * DQ;
+  // per query tile: per-warp gate votes u32 [2 parity][4 warps]
+  static constexpr int XCH_TILE = 2 * 4 * 4;
+  static constexpr int OFF_XCH = (OFF_BAR + NUM_BARS * 8 + 15) / 16 * 16;  // 16-B aligned: votes read as v4
+  static constexpr int OFF_DEC = OFF_XCH + NQ * XCH_TILE;   // u32 [NQ][DQ] decision ring (V producer)
   static constexpr int OFF_DECM = OFF_DEC + NQ * DQ * 4;    // u32 [NQ] decision of the current step (MMA)
   static constexpr int OFF_TMEMPTR = OFF_DECM + NQ * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
@@ -122,11 +124,19 @@ struct KCfg {
   static constexpr int S_COL = CALIB ? 0 : NQ * D;         // S_s at S_COL + s * 128
   static constexpr int TMEM_NEED = S_COL + NQ * 128;
   static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
+  // one thread per row: warpgroup s is query tile s; the last warpgroup holds
+  // the K producer, the MMA issuer, the V producer and one idle warp
   static constexpr int SOFTMAX_WARPS = 4 * NQ;
   static constexpr int KPROD_WARP = SOFTMAX_WARPS;
   static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static constexpr int VPROD_WARP = SOFTMAX_WARPS + 2;
-  static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 3) * 32;
+  static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 4) * 32;
+  // register split (setmaxnreg): softmax warps hold a 128-column score row,
+  // its exponentials and the packed P row
+  static constexpr int REG_OTHER = 56;
+  static constexpr int REG_SOFT_MAX = (65536 - 128 * REG_OTHER) / (SOFTMAX_WARPS * 32) / 8 * 8;
+  static constexpr int REG_SOFT = REG_SOFT_MAX > 248 ? 248 : REG_SOFT_MAX;
+  static constexpr bool SPLIT_REGS = true;
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
   static_assert(NQ == 1 || NQ == 2, "one or two query tiles per CTA");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -162,11 +172,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   uint64_t* v_full = k_empty + KS;
   uint64_t* v_empty = v_full + VS;
   uint64_t* s_full = v_empty + VS;  // [NQ] QK_s(j) landed (and every earlier MMA)
-  uint64_t* p_full = s_full + NQ;   // [NQ] softmax s done with step j (P written, O rescaled)
-  uint64_t* o_full = p_full + NQ;   // [NQ] last PV_s landed
+  uint64_t* p_full = s_full + NQ;   // [NQ][2] P half written (half 0 also: O_s rescaled)
+  uint64_t* o_full = p_full + 2 * NQ;  // [NQ] last PV_s landed
   uint64_t* dec_full = o_full + NQ; // [NQ][DQ]
   uint64_t* dec_empty = dec_full + NQ * DQ;
-  const uint32_t vote_sm = smem_u32(smem + C::OFF_VOTE);
+  const uint32_t xch_sm = smem_u32(smem + C::OFF_XCH);
   const uint32_t dec_sm = smem_u32(smem + C::OFF_DEC);
   const uint32_t decm_sm = smem_u32(smem + C::OFF_DECM);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
@@ -204,7 +214,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);  // the 4 warps of softmax group s
+      mbar_init(&p_full[2 * s], 4);  // the 4 softmax warps of query tile s
+      mbar_init(&p_full[2 * s + 1], 4);
       mbar_init(&o_full[s], 1);
     }
     for (int i = 0; i < NQ * DQ; ++i) {
@@ -224,8 +235,12 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
-
+  // Register split: setmaxnreg inside each role (the regions must not merge,
+  // or ptxas allocates the merged code at the smaller budget).  Every role
+  // leaves through bsfa_role_exit: arrive on the teardown barrier; the MMA
+  // warp waits for everyone there and frees TMEM.
   if (warp == C::KPROD_WARP) {
+    if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
     // ======================= TMA producer: Q, K (warp-convergent, one elected issuer)
     if (nsteps > 0) {
       if (lane == 0) {
@@ -248,7 +263,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       }
     }
     __syncwarp();
+    named_bar_arrive(15, C::NUM_THREADS);
+    return;
   } else if (warp == C::VPROD_WARP) {
+    if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
     // ======================= TMA producer: V gate tiles kept by some query tile =========
     if constexpr (!CALIB) {
       if (nsteps > 0) {
@@ -296,7 +314,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       }
     }
     __syncwarp();
+    named_bar_arrive(15, C::NUM_THREADS);
+    return;
   } else if (warp == C::MMA_WARP) {
+    if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
     // ======================= MMA issuer (warp-convergent, one elected issuer) ==========
     if (nsteps > 0) {
       constexpr uint32_t IDESC_QK = make_idesc_bf16(128, 128, 0, 0);
@@ -329,34 +350,39 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         unsigned uidx[GT];
 #pragma unroll
         for (int s = 0; s < NQ; ++s) {
-          mbar_wait(&p_full[s], j & 1);
-          if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps)
-            p.trace[(kEvPSeen * 2 + s) * kTraceSteps + j] = clock64();
-          tc_fence_after();
-          if constexpr (!CALIB) {
-            uint32_t bits;
-            if (kind == kStepAll) bits = kAllBits;
-            else if (kind == kStepNone) bits = 0;
-            else bits = lds_u32(decm_sm + s * 4);
+          // P of tile s arrives per 64-key half; the PV of half 0 runs while
+          // the softmax computes half 1
+          uint32_t bits = 0;
 #pragma unroll
-            for (int h = 0; h < GT; ++h) {
-              if ((bits >> h) & 1u) {
-                if (!((prev >> h) & 1u)) uidx[h] = vbase + nunits++;
-                const unsigned u = uidx[h];
-                const int slot = int(u % VS);
-                mbar_wait(&v_full[slot], (u / VS) & 1);
-                if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps)
-                  p.trace[(kEvVReady * 2 + s) * kTraceSteps + j] = clock64();
-                tc_fence_after();
-                const uint64_t dv = dv0 + uint64_t((slot * C::V_UNIT) >> 4);
-#pragma unroll
-                for (int q = 0; q < BN / 64; ++q) {  // 64 keys per batch of 4 MMAs
-                  umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::S_COL + s * 128 + h * (BN / 2) + q * 32,
-                              dv + uint64_t(q * 512), IDESC_PV, (o_started >> s) & 1u);
-                  o_started |= 1u << s;
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&p_full[2 * s + hh], j & 1);
+            if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps && hh == 0)
+              p.trace[(kEvPSeen * 2 + s) * kTraceSteps + j] = clock64();
+            tc_fence_after();
+            if constexpr (!CALIB) {
+              if (hh == 0) {
+                if (kind == kStepAll) bits = kAllBits;
+                else if (kind == kStepNone) bits = 0;
+                else bits = lds_u32(decm_sm + s * 4);
+              }
+              const int x = GT == 2 ? hh : 0;  // gate tile of this half
+              if ((bits >> x) & 1u) {
+                if (hh == 0 || GT == 2) {
+                  if (!((prev >> x) & 1u)) uidx[x] = vbase + nunits++;
+                  const unsigned u = uidx[x];
+                  mbar_wait(&v_full[u % VS], (u / VS) & 1);
+                  if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps)
+                    p.trace[(kEvVReady * 2 + s) * kTraceSteps + j] = clock64();
                 }
+                const uint64_t dv = dv0 + uint64_t(((uidx[x] % VS) * C::V_UNIT) >> 4) +
+                                    uint64_t(GT == 1 ? hh * 512 : 0);  // 64 key rows = 8 KB
+                umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::S_COL + s * 128 + hh * 32, dv, IDESC_PV,
+                            (o_started >> s) & 1u);
+                o_started |= 1u << s;
               }
             }
+          }
+          if constexpr (!CALIB) {
             prev |= bits;
             if (s == NQ - 1) {
               // every PV reading this step's V units has been issued
@@ -374,8 +400,18 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       }
     }
     __syncwarp();
+    named_bar_sync(15, C::NUM_THREADS);
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+    return;
   } else if (warp < C::SOFTMAX_WARPS) {
-    // ======================= softmax group s =======================
+    if constexpr (C::SPLIT_REGS) setmaxnreg_inc<C::REG_SOFT>();
+    // ======================= softmax group s (query tile s) =======================
+    // Thread r owns row r (TMEM lane r) over all 128 keys of a step.  Critical
+    // path per step: S -> registers, gate-tile maxima, gate vote, then per
+    // 64-key half: exponentials -> packed P in TMEM -> signal the MMA warp
+    // (the PV of half 0 overlaps the exponentials of half 1).  The row sum is
+    // accumulated after P is released.
     const int s = warp >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;  // row inside the query tile == TMEM lane
@@ -384,8 +420,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     const uint32_t s_row = tmem + lane_off + C::S_COL + s * 128;
     const uint32_t o_row = tmem + lane_off + C::O_COL + s * D;
     const float sl2 = p.scale_log2;
-    const uint32_t vote_base = vote_sm + s * 8 * 4;
+    const float scale = p.scale;
+    const float rescale_raw = p.rescale_raw;
+    const uint32_t xvote = xch_sm + s * C::XCH_TILE;  // u32 [2 parity][4 warps]
     const bool tr0 = BSFA_TRACE && tr_cta && r == 0;
+    uint64_t* p_half = p_full + 2 * s;
 
     float T = 0.f;
     if (!CALIB && p.gate_mode == kGateThreshold) {
@@ -395,7 +434,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
 
     float m_ref = -INFINITY;  // raw (unscaled) reference max of this row over its kept tiles
     float l_sum = 0.f;        // row sum relative to m_ref
-    bool o_valid = false;     // group-uniform: O_s holds data
+    bool o_valid = false;     // tile-uniform: O_s holds data
     unsigned dn = 0;
     unsigned long long kept_tiles = 0;
 
@@ -407,6 +446,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
+      if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();
 
       const int kind = CALIB ? kStepDynamic : step_kind(p, j, qi);
       if (!CALIB) {
@@ -421,42 +461,52 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
             if (j * 128 + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
         }
       }
-      // row max per gate tile (three-input FMNMX)
-      float mx[GT];
+      // row max per 64-key half (three-input FMNMX, four chains each)
+      float mh[2];
 #pragma unroll
-      for (int h = 0; h < GT; ++h) {
-        const uint32_t* x = sv + h * BN;
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t* x = sv + hh * 64;
         float a0 = fmax3(__uint_as_float(x[0]), __uint_as_float(x[1]), __uint_as_float(x[2]));
         float a1 = fmax3(__uint_as_float(x[3]), __uint_as_float(x[4]), __uint_as_float(x[5]));
         float a2 = fmax3(__uint_as_float(x[6]), __uint_as_float(x[7]), __uint_as_float(x[8]));
         float a3 = fmax3(__uint_as_float(x[9]), __uint_as_float(x[10]), __uint_as_float(x[11]));
 #pragma unroll
-        for (int c = 12; c + 8 <= BN; c += 8) {
+        for (int c = 12; c < 60; c += 8) {
           a0 = fmax3(a0, __uint_as_float(x[c]), __uint_as_float(x[c + 1]));
           a1 = fmax3(a1, __uint_as_float(x[c + 2]), __uint_as_float(x[c + 3]));
           a2 = fmax3(a2, __uint_as_float(x[c + 4]), __uint_as_float(x[c + 5]));
           a3 = fmax3(a3, __uint_as_float(x[c + 6]), __uint_as_float(x[c + 7]));
         }
-        // BN % 8 == 0 and 12 + 8k covers up to BN - 4: fold the last 4
-        a0 = fmax3(a0, __uint_as_float(x[BN - 4]), __uint_as_float(x[BN - 3]));
-        a1 = fmax3(a1, __uint_as_float(x[BN - 2]), __uint_as_float(x[BN - 1]));
-        mx[h] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+        a0 = fmax3(a0, __uint_as_float(x[60]), __uint_as_float(x[61]));
+        a1 = fmax3(a1, __uint_as_float(x[62]), __uint_as_float(x[63]));
+        mh[hh] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+      }
+      // gate-tile maxima: b_n = 64 -> the halves; b_n = 128 -> the whole row
+      float mx[GT];
+      if constexpr (GT == 2) {
+        mx[0] = mh[0];
+        mx[1] = mh[1];
+      } else {
+        mx[0] = fmaxf(mh[0], mh[1]);
       }
 
       if constexpr (CALIB) {
 #pragma unroll
-        for (int h = 0; h < GT; ++h) {
-          float m = mx[h];
+        for (int x = 0; x < GT; ++x) {
+          float m = mx[x];
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-          if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * GT + h], float_to_ordered(m * p.scale));
+          if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * GT + x], float_to_ordered(m * scale));
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[s]);
+        if (lane == 0) {
+          mbar_arrive(&p_half[0]);
+          mbar_arrive(&p_half[1]);
+        }
         continue;
       } else {
-        // ---- gate: OR over the group's 128 rows of (rowmax * scale > T)
+        // ---- gate: OR over the tile's 128 rows of (rowmax * scale > T)
         uint32_t bits;
         if (kind == kStepAll) {
           bits = kAllBits;
@@ -465,11 +515,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         } else {
           uint32_t wv = 0;
 #pragma unroll
-          for (int h = 0; h < GT; ++h) wv |= (__ballot_sync(0xffffffffu, mx[h] * p.scale > T) != 0u ? 1u : 0u) << h;
+          for (int x = 0; x < GT; ++x) wv |= (__ballot_sync(0xffffffffu, mx[x] * scale > T) != 0u ? 1u : 0u) << x;
           const uint32_t par = j & 1;
-          if (lane == 0) sts_u32(vote_base + (par * 4 + wq) * 4, wv);
+          if (lane == 0) sts_u32(xvote + (par * 4 + wq) * 4, wv);
           named_bar_sync(1 + s, 128);
-          const uint4 v4 = lds_u128(vote_base + par * 4 * 4);
+          const uint4 v4 = lds_u128(xvote + par * 16);
           bits = v4.x | v4.y | v4.z | v4.w;
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvVoted * 2 + s) * kTraceSteps + j] = clock64();
@@ -485,75 +535,38 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           if (p.decisions) {
             int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi) * p.gate_cols;
 #pragma unroll
-            for (int h = 0; h < GT; ++h)
-              drow[j * GT + h] = j == qi ? int8_t(2) : (((bits >> h) & 1u) ? int8_t(3) : int8_t(1));
+            for (int x = 0; x < GT; ++x)
+              drow[j * GT + x] = j == qi ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
           }
         }
         if (kind == kStepDynamic) ++dn;
         if (bits == 0) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[s]);
+          if (lane == 0) {
+            mbar_arrive(&p_half[0]);
+            mbar_arrive(&p_half[1]);
+          }
           if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
           continue;
         }
 
         float m_step = -INFINITY;
 #pragma unroll
-        for (int h = 0; h < GT; ++h)
-          if ((bits >> h) & 1u) m_step = fmaxf(m_step, mx[h]);
+        for (int x = 0; x < GT; ++x)
+          if ((bits >> x) & 1u) m_step = fmaxf(m_step, mx[x]);
         const float m_new = fmaxf(m_ref, m_step);
         float alpha = 1.f;
         bool rescale = false;
         if (!o_valid) {
           m_ref = m_new;
-        } else if (m_new > m_ref + p.rescale_raw) {
+        } else if (m_new > m_ref + rescale_raw) {
           alpha = ex2_approx((m_ref - m_new) * sl2);
           m_ref = m_new;
           rescale = true;
         }
-
-        // P = exp2(s * scale*log2e - m * scale*log2e), bf16-packed over S_s
-        const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
-        const uint64_t sl2x2 = f2_pack(sl2, sl2);
-        const uint64_t negx2 = f2_pack(neg, neg);
-        uint64_t acc0 = 0, acc1 = 0;
-#pragma unroll
-        for (int h = 0; h < GT; ++h) {
-          if (!((bits >> h) & 1u)) continue;
-#pragma unroll
-          for (int cb = 0; cb < BN; cb += 32) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              const int e = h * BN + cb + c;
-              const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2, negx2);
-              const uint64_t x1 =
-                  ffma2(f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])), sl2x2, negx2);
-              const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
-              float p2, p3;
-              // offload part of the exponentials from the MUFU to the FMA pipe
-              if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
-                const uint64_t e1 = exp2_poly_x2(x1);
-                p2 = f2_lo(e1);
-                p3 = f2_hi(e1);
-              } else {
-                p2 = ex2_approx(f2_lo(x1));
-                p3 = ex2_approx(f2_hi(x1));
-              }
-              acc0 = fadd2(acc0, f2_pack(p0, p1));
-              acc1 = fadd2(acc1, f2_pack(p2, p3));
-              pk[c / 2] = pack_bf16x2(p0, p1);
-              pk[c / 2 + 1] = pack_bf16x2(p2, p3);
-            }
-            tmem_st16(s_row + (h * BN + cb) / 2, pk);
-          }
-        }
-        const uint64_t acc = fadd2(acc0, acc1);
-        l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
-
-        // O_s is quiescent here (S_s(j) committed after PV_s(j-1)): rescale
-        // the rows whose reference max moved by more than 2^8
+        // O_s is quiescent here (S_s(j) committed after PV_s(j-1)): rescale the
+        // rows whose reference max moved by more than 2^8, before any P release
         if (__any_sync(0xffffffffu, rescale)) {
           const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
@@ -570,11 +583,68 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
             tmem_st32(o_row + c, ov);
           }
         }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[s]);
+
+        // P = exp2(s * scale*log2e - m * scale*log2e), per 64-key half, bf16-packed
+        // over S_s columns [32hh, 32hh + 32); released to the MMA warp per half
+        const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
+        const uint64_t sl2x2 = f2_pack(sl2, sl2);
+        const uint64_t negx2 = f2_pack(neg, neg);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const bool kept_h = ((bits >> (GT == 2 ? hh : 0)) & 1u) != 0;
+          if (kept_h) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) {
+              const int e = hh * 64 + c;
+              const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2, negx2);
+              const uint64_t x1 =
+                  ffma2(f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])), sl2x2, negx2);
+              const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
+              float p2, p3;
+              // offload part of the exponentials from the MUFU to the FMA pipe
+              if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
+                const uint64_t e1 = exp2_poly_x2(x1);
+                p2 = f2_lo(e1);
+                p3 = f2_hi(e1);
+              } else {
+                p2 = ex2_approx(f2_lo(x1));
+                p3 = ex2_approx(f2_hi(x1));
+              }
+              sv[e] = __float_as_uint(p0);
+              sv[e + 1] = __float_as_uint(p1);
+              sv[e + 2] = __float_as_uint(p2);
+              sv[e + 3] = __float_as_uint(p3);
+              pk[c / 2] = pack_bf16x2(p0, p1);
+              pk[c / 2 + 1] = pack_bf16x2(p2, p3);
+            }
+            tmem_st32(s_row + hh * 32, pk);
+            tmem_wait_st();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_half[hh]);
+        }
         if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
+
+        // row sum of the kept exponentials (off the MMA critical path)
+        uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (((bits >> (GT == 2 ? hh : 0)) & 1u) != 0) {
+#pragma unroll
+            for (int c = 0; c < 64; c += 8) {
+              const int e = hh * 64 + c;
+              acc0 = fadd2(acc0, f2_pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])));
+              acc1 = fadd2(acc1, f2_pack(__uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3])));
+              acc2 = fadd2(acc2, f2_pack(__uint_as_float(sv[e + 4]), __uint_as_float(sv[e + 5])));
+              acc3 = fadd2(acc3, f2_pack(__uint_as_float(sv[e + 6]), __uint_as_float(sv[e + 7])));
+            }
+          }
+        }
+        const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
+        l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
+        if (tr0 && j < kTraceSteps) p.trace[(kEvExpDone * 2 + s) * kTraceSteps + j] = clock64();
         o_valid = true;
       }
     }
@@ -654,7 +724,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
       }
-      p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * p.scale + logf(l_sum);
+      p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
       if (bad && p.status) atomicOr(p.status, 1);
       if (r == 0 && p.counters) {
         atomicAdd(&p.counters[0], (unsigned long long)nsteps * GT);
@@ -662,12 +732,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       }
     }
     tc_fence_before();
-  }
-
-  __syncthreads();
-  if (warp == C::MMA_WARP) {
-    tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    named_bar_arrive(15, C::NUM_THREADS);
+    return;
+  } else {
+    // idle warp (completes the last warpgroup for setmaxnreg)
+    if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
+    named_bar_arrive(15, C::NUM_THREADS);
+    return;
   }
 }
 

@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
-EV = ["SReady", "Voted", "PDone", "PSeen", "VReady", "Issued"]
+EV = ["SReady", "Voted", "PDone", "PSeen", "VReady", "Issued", "LdDone", "ExpDone"]
 STEPS = 2048
 
 
@@ -52,7 +52,10 @@ def run(mode, seq=32768, cta=0):
     base = ev["SReady"][0][0]
     out = {"steps": n}
     for s in range(2):
-        sr, vo, pd, ps, vr, iss = (ev[x][s] for x in EV)
+        sr, vo, pd, ps, vr, iss, ld, ex = (ev[x][s] for x in EV)
+        out[f"s{s}_ld(S->LdDone)"] = float(np.median(ld - sr))
+        out[f"s{s}_exp(Voted->ExpDone)"] = float(np.median(ex - vo))
+        out[f"s{s}_wait_st(ExpDone->PDone)"] = float(np.median(pd - ex))
         out[f"s{s}_softmax(S->Pdone)"] = float(np.median(pd - sr))
         out[f"s{s}_vote(S->Voted)"] = float(np.median(vo - sr))
         out[f"s{s}_mma_lag(Pdone->Pseen)"] = float(np.median(ps - pd))
