@@ -44,6 +44,10 @@
 #ifndef BSFA_EXP_EMU
 #define BSFA_EXP_EMU 1
 #endif
+// Order the polynomial exponentials after the same group's MUFU exponentials.
+#ifndef BSFA_EXP_CHAIN
+#define BSFA_EXP_CHAIN 1
+#endif
 // Debug timeline (bsfa_debug_trace); compiled out of the production library.
 #ifndef BSFA_TRACE
 #define BSFA_TRACE 0
@@ -160,25 +164,28 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   constexpr uint32_t kAllBits = (1u << GT) - 1u;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem + C::OFF_Q;
-  uint8_t* sK = smem + C::OFF_K;
-  uint8_t* sV = smem + C::OFF_V;
+  // all shared-memory addresses are 32-bit shared-window offsets computed once
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const uint32_t sQ = sbase + C::OFF_Q;
+  const uint32_t sK = sbase + C::OFF_K;
+  const uint32_t sV = sbase + C::OFF_V;
   int* cvals = reinterpret_cast<int*>(smem + C::OFF_CAL);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* bar_q = bars;
-  uint64_t* k_full = bar_q + 1;
-  uint64_t* k_empty = k_full + KS;
-  uint64_t* v_full = k_empty + KS;
-  uint64_t* v_empty = v_full + VS;
-  uint64_t* s_full = v_empty + VS;  // [NQ] QK_s(j) landed (and every earlier MMA)
-  uint64_t* p_full = s_full + NQ;   // [NQ][2] P half written (half 0 also: O_s rescaled)
-  uint64_t* o_full = p_full + 2 * NQ;  // [NQ] last PV_s landed
-  uint64_t* dec_full = o_full + NQ; // [NQ][DQ]
-  uint64_t* dec_empty = dec_full + NQ * DQ;
-  const uint32_t xch_sm = smem_u32(smem + C::OFF_XCH);
-  const uint32_t dec_sm = smem_u32(smem + C::OFF_DEC);
-  const uint32_t decm_sm = smem_u32(smem + C::OFF_DECM);
+  // mbarriers (8 bytes each)
+  const uint32_t bar_q = sbase + C::OFF_BAR;
+  const uint32_t k_full = bar_q + 8;              // [KS]
+  const uint32_t k_empty = k_full + 8 * KS;       // [KS]
+  const uint32_t v_full = k_empty + 8 * KS;       // [VS]
+  const uint32_t v_empty = v_full + 8 * VS;       // [VS]
+  const uint32_t s_full = v_empty + 8 * VS;       // [NQ] QK_s(j) landed (and every earlier MMA)
+  const uint32_t p_full = s_full + 8 * NQ;        // [NQ][2] P half written (half 0 also: O_s rescaled)
+  const uint32_t o_full = p_full + 16 * NQ;       // [NQ] last PV_s landed
+  const uint32_t dec_full = o_full + 8 * NQ;      // [NQ][DQ]
+  const uint32_t dec_empty = dec_full + 8 * NQ * DQ;
+  const uint32_t xch_sm = sbase + C::OFF_XCH;
+  const uint32_t dec_sm = sbase + C::OFF_DEC;
+  const uint32_t decm_sm = sbase + C::OFF_DECM;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -205,22 +212,22 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   if (warp == C::KPROD_WARP && lane == 0) {
     mbar_init(bar_q, 1);
     for (int i = 0; i < KS; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+      mbar_init((k_full + 8 * (i)), 1);
+      mbar_init((k_empty + 8 * (i)), 1);
     }
     for (int i = 0; i < VS; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init((v_full + 8 * (i)), 1);
+      mbar_init((v_empty + 8 * (i)), 1);
     }
     for (int s = 0; s < NQ; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[2 * s], 4);  // the 4 softmax warps of query tile s
-      mbar_init(&p_full[2 * s + 1], 4);
-      mbar_init(&o_full[s], 1);
+      mbar_init((s_full + 8 * (s)), 1);
+      mbar_init((p_full + 8 * (2 * s)), 4);  // the 4 softmax warps of query tile s
+      mbar_init((p_full + 8 * (2 * s + 1)), 4);
+      mbar_init((o_full + 8 * (s)), 1);
     }
     for (int i = 0; i < NQ * DQ; ++i) {
-      mbar_init(&dec_full[i], 1);
-      mbar_init(&dec_empty[i], 1);
+      mbar_init((dec_full + 8 * (i)), 1);
+      mbar_init((dec_empty + 8 * (i)), 1);
     }
     fence_mbarrier_init();
   }
@@ -255,11 +262,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           tma_load_4d_w(sQ + s * C::Q_TILE + c * 128 * 128, &tm_q, bar_q, c * 64, qi * 128, hq0 + s, b, kEvictFirst);
       for (int j = 0; j < nsteps; ++j) {
         const int st = j % KS;
-        mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
-        mbar_arrive_expect_tx_w(&k_full[st], C::K_TILE);
+        mbar_wait((k_empty + 8 * (st)), ((j / KS) & 1) ^ 1);
+        mbar_arrive_expect_tx_w((k_full + 8 * (st)), C::K_TILE);
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d_w(sK + st * C::K_TILE + c * 128 * 128, &tm_k, &k_full[st], c * 64, j * 128, g, b, kEvictLast);
+          tma_load_4d_w(sK + st * C::K_TILE + c * 128 * 128, &tm_k, (k_full + 8 * (st)), c * 64, j * 128, g, b, kEvictLast);
       }
     }
     __syncwarp();
@@ -274,11 +281,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         unsigned vcount = 0, dn = 0;
         auto load_unit = [&](int j, int h) {
           const int slot = int(vcount % VS);
-          mbar_wait(&v_empty[slot], ((vcount / VS) & 1) ^ 1);
-          mbar_arrive_expect_tx_w(&v_full[slot], C::V_UNIT);
+          mbar_wait((v_empty + 8 * (slot)), ((vcount / VS) & 1) ^ 1);
+          mbar_arrive_expect_tx_w((v_full + 8 * (slot)), C::V_UNIT);
 #pragma unroll
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_4d_w(sV + slot * C::V_UNIT + c * BN * 128, &tm_v, &v_full[slot], c * 64, j * 128 + h * BN, g, b,
+            tma_load_4d_w(sV + slot * C::V_UNIT + c * BN * 128, &tm_v, (v_full + 8 * (slot)), c * 64, j * 128 + h * BN, g, b,
                           kEvictLast);
           ++vcount;
         };
@@ -295,10 +302,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
             const uint32_t ph = (dn / DQ) & 1;
 #pragma unroll
             for (int s = 0; s < NQ; ++s) {
-              mbar_wait(&dec_full[s * DQ + di], ph);
+              mbar_wait((dec_full + 8 * (s * DQ + di)), ph);
               const uint32_t w = lds_u32(dec_sm + (s * DQ + di) * 4);
               __syncwarp();
-              mbar_arrive_w(&dec_empty[s * DQ + di]);
+              mbar_arrive_w((dec_empty + 8 * (s * DQ + di)));
 #pragma unroll
               for (int h = 0; h < GT; ++h)
                 if (((w & ~prev) >> h) & 1u) load_unit(j, h);
@@ -323,19 +330,19 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       constexpr uint32_t IDESC_QK = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t IDESC_PV = make_idesc_bf16(128, D, 0, 1);
       // descriptor templates; per-MMA offsets only touch the 14-bit start-address field
-      const uint64_t dq0 = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
-      const uint64_t dk0 = make_sdesc_sw128(smem_u32(sK), 16, 1024);
-      const uint64_t dv0 = make_sdesc_sw128(smem_u32(sV), BN * 128, 1024);
+      const uint64_t dq0 = make_sdesc_sw128(sQ, 16, 1024);
+      const uint64_t dk0 = make_sdesc_sw128(sK, 16, 1024);
+      const uint64_t dv0 = make_sdesc_sw128(sV, BN * 128, 1024);
       mbar_wait(bar_q, 0);
 
       auto issue_qk = [&](int s, int j) {
         const int st = j % KS;
-        if (s == 0) mbar_wait(&k_full[st], (j / KS) & 1);
+        if (s == 0) mbar_wait((k_full + 8 * (st)), (j / KS) & 1);
         tc_fence_after();
         umma_qk_tile_w<D, 128>(tmem + C::S_COL + s * 128, dq0 + uint64_t((s * C::Q_TILE) >> 4),
                                dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
-        if (s == NQ - 1) umma_commit_w(&k_empty[st]);
-        umma_commit_w(&s_full[s]);
+        if (s == NQ - 1) umma_commit_w((k_empty + 8 * (st)));
+        umma_commit_w((s_full + 8 * (s)));
       };
 
 #pragma unroll
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           uint32_t bits = 0;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            mbar_wait(&p_full[2 * s + hh], j & 1);
+            mbar_wait((p_full + 8 * (2 * s + hh)), j & 1);
             if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps && hh == 0)
               p.trace[(kEvPSeen * 2 + s) * kTraceSteps + j] = clock64();
             tc_fence_after();
@@ -370,7 +377,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
                 if (hh == 0 || GT == 2) {
                   if (!((prev >> x) & 1u)) uidx[x] = vbase + nunits++;
                   const unsigned u = uidx[x];
-                  mbar_wait(&v_full[u % VS], (u / VS) & 1);
+                  mbar_wait((v_full + 8 * (u % VS)), (u / VS) & 1);
                   if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps)
                     p.trace[(kEvVReady * 2 + s) * kTraceSteps + j] = clock64();
                 }
@@ -386,10 +393,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
             prev |= bits;
             if (s == NQ - 1) {
               // every PV reading this step's V units has been issued
-              for (unsigned x = 0; x < nunits; ++x) umma_commit_w(&v_empty[(vbase + x) % VS]);
+              for (unsigned x = 0; x < nunits; ++x) umma_commit_w((v_empty + 8 * ((vbase + x) % VS)));
               vbase += nunits;
             }
-            if (j == nsteps - 1) umma_commit_w(&o_full[s]);
+            if (j == nsteps - 1) umma_commit_w((o_full + 8 * (s)));
           }
           // QK_s(j+1) reuses S_s; issued after PV_s(j), so its commit also
           // certifies that PV_s(j) has landed (softmax may rescale O_s)
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     const float rescale_raw = p.rescale_raw;
     const uint32_t xvote = xch_sm + s * C::XCH_TILE;  // u32 [2 parity][4 warps]
     const bool tr0 = BSFA_TRACE && tr_cta && r == 0;
-    uint64_t* p_half = p_full + 2 * s;
+    const uint32_t p_half = p_full + 16 * s;
 
     float T = 0.f;
     if (!CALIB && p.gate_mode == kGateThreshold) {
@@ -439,14 +446,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     unsigned long long kept_tiles = 0;
 
     for (int j = 0; j < nsteps; ++j) {
-      mbar_wait(&s_full[s], j & 1);
+      mbar_wait((s_full + 8 * (s)), j & 1);
       if (tr0 && j < kTraceSteps) p.trace[(kEvSReady * 2 + s) * kTraceSteps + j] = clock64();
       tc_fence_after();
       uint32_t sv[128];
 #pragma unroll
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
-      if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();
 
       const int kind = CALIB ? kStepDynamic : step_kind(p, j, qi);
       if (!CALIB) {
@@ -481,6 +487,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         a1 = fmax3(a1, __uint_as_float(x[62]), __uint_as_float(x[63]));
         mh[hh] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
       }
+      if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();  // max done
       // gate-tile maxima: b_n = 64 -> the halves; b_n = 128 -> the whole row
       float mx[GT];
       if constexpr (GT == 2) {
@@ -501,8 +508,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&p_half[0]);
-          mbar_arrive(&p_half[1]);
+          mbar_arrive((p_half + 8 * (0)));
+          mbar_arrive((p_half + 8 * (1)));
         }
         continue;
       } else {
@@ -526,9 +533,9 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         if (r == 0) {
           if (kind == kStepDynamic) {
             const int di = int(dn % DQ);
-            mbar_wait(&dec_empty[s * DQ + di], ((dn / DQ) & 1) ^ 1);
+            mbar_wait((dec_empty + 8 * (s * DQ + di)), ((dn / DQ) & 1) ^ 1);
             sts_u32(dec_sm + (s * DQ + di) * 4, bits);
-            mbar_arrive(&dec_full[s * DQ + di]);
+            mbar_arrive((dec_full + 8 * (s * DQ + di)));
           }
           sts_u32(decm_sm + s * 4, bits);
           kept_tiles += __popc(bits);
@@ -544,8 +551,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(&p_half[0]);
-            mbar_arrive(&p_half[1]);
+            mbar_arrive((p_half + 8 * (0)));
+            mbar_arrive((p_half + 8 * (1)));
           }
           if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
           continue;
@@ -604,7 +611,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
               float p2, p3;
               // offload part of the exponentials from the MUFU to the FMA pipe
               if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
-                const uint64_t e1 = exp2_poly_x2(x1);
+                // x1 += 0 * (p0, p1): a data dependency on this group's MUFU
+                // results, so the scheduler interleaves the polynomial work with
+                // the (8-cycle) MUFU issue slots instead of clustering the MUFUs
+                const uint64_t x1d = BSFA_EXP_CHAIN ? ffma2(f2_pack(p0, p1), 0ull, x1) : x1;
+                const uint64_t e1 = exp2_poly_x2(x1d);
                 p2 = f2_lo(e1);
                 p3 = f2_hi(e1);
               } else {
@@ -623,7 +634,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_half[hh]);
+          if (lane == 0) mbar_arrive((p_half + 8 * (hh)));
+          if (tr0 && hh == 0 && j < kTraceSteps) p.trace[(kEvExpDone * 2 + s) * kTraceSteps + j] = clock64();
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
 
@@ -644,7 +656,6 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         }
         const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
         l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
-        if (tr0 && j < kTraceSteps) p.trace[(kEvExpDone * 2 + s) * kTraceSteps + j] = clock64();
         o_valid = true;
       }
     }
@@ -701,7 +712,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       }
     } else {
       // ---- epilogue: O = O~ / l, lse = m * scale + ln l (engine.py:178-182)
-      mbar_wait(&o_full[s], 0);
+      mbar_wait((o_full + 8 * (s)), 0);
       tc_fence_after();
       const float inv_l = 1.f / l_sum;
       bool bad = !(l_sum > 0.f);

@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
-EV = ["SReady", "Voted", "PDone", "PSeen", "VReady", "Issued", "LdDone", "ExpDone"]
+EV = ["SReady", "Voted", "PDone", "PSeen", "VReady", "Issued", "MaxDone", "Half0"]
 STEPS = 2048
 
 
@@ -53,9 +53,11 @@ def run(mode, seq=32768, cta=0):
     out = {"steps": n}
     for s in range(2):
         sr, vo, pd, ps, vr, iss, ld, ex = (ev[x][s] for x in EV)
-        out[f"s{s}_ld(S->LdDone)"] = float(np.median(ld - sr))
-        out[f"s{s}_exp(Voted->ExpDone)"] = float(np.median(ex - vo))
-        out[f"s{s}_wait_st(ExpDone->PDone)"] = float(np.median(pd - ex))
+        out[f"s{s}_ldmax(S->MaxDone)"] = float(np.median(ld - sr))
+        out[f"s{s}_vote(MaxDone->Voted)"] = float(np.median(vo - ld))
+        kept0 = ex > 0
+        out[f"s{s}_half0(Voted->Half0 arrive)"] = float(np.median((ex - vo)[kept0])) if kept0.any() else -1
+        out[f"s{s}_half1(Half0->PDone)"] = float(np.median((pd - ex)[kept0])) if kept0.any() else -1
         out[f"s{s}_softmax(S->Pdone)"] = float(np.median(pd - sr))
         out[f"s{s}_vote(S->Voted)"] = float(np.median(vo - sr))
         out[f"s{s}_mma_lag(Pdone->Pseen)"] = float(np.median(ps - pd))
