@@ -107,7 +107,10 @@ struct KCfg {
   static constexpr int V_UNIT = BN * D * 2;   // one gate tile of V
   static constexpr int KS = D == 128 ? 2 : 3;
   static constexpr int VS = CALIB ? 0 : (D == 128 ? 81920 : 65536) / V_UNIT;
-  static constexpr int DQ = 4;                // decision ring depth (dynamic steps)
+#ifndef BSFA_DQ
+#define BSFA_DQ 4
+#endif
+  static constexpr int DQ = BSFA_DQ;          // decision ring depth (dynamic steps)
   static constexpr int MAXA = 4096;           // calibration: max off-frontier gate tiles per row
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQ * Q_TILE;
@@ -149,9 +152,9 @@ struct KCfg {
 };
 
 // Static decision of step j (identical in every role).
-__device__ __forceinline__ int step_kind(const KernelParams& p, int j, int qi) {
-  if (j == qi || p.gate_mode == kGateDense) return kStepAll;  // frontier (tiling.py:50-60) / DenseGate
-  if (p.gate_mode == kGateFrontier) return kStepNone;          // FrontierOnlyGate
+__device__ __forceinline__ int step_kind(int gate_mode, int j, int qi) {
+  if (j == qi || gate_mode == kGateDense) return kStepAll;  // frontier (tiling.py:50-60) / DenseGate
+  if (gate_mode == kGateFrontier) return kStepNone;          // FrontierOnlyGate
   return kStepDynamic;
 }
 
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   // all shared-memory addresses are 32-bit shared-window offsets computed once
   const uint32_t sraw = smem_u32(smem_raw);
-  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t sbase = opaque_u32((sraw + 1023u) & ~1023u);
   uint8_t* smem = smem_raw + (sbase - sraw);
   const uint32_t sQ = sbase + C::OFF_Q;
   const uint32_t sK = sbase + C::OFF_K;
@@ -206,6 +209,9 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   // 128-key steps: causal -> through the frontier step i; calibration -> the
   // off-frontier prefix only (calibration.py:110-113)
   const int nsteps = CALIB ? qi : (p.causal ? qi + 1 : p.num_steps);
+  const int gate_mode = p.gate_mode;
+  const bool causal = p.causal != 0;
+  const int valid_len = p.valid_len;
   const bool tr_cta = BSFA_TRACE && p.trace && (int)blockIdx.x == p.trace_cta;
 
   // ---- setup
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           ++vcount;
         };
         for (int j = 0; j < nsteps; ++j) {
-          const int kind = step_kind(p, j, qi);
+          const int kind = step_kind(gate_mode, j, qi);
           if (kind == kStepAll) {
 #pragma unroll
             for (int h = 0; h < GT; ++h) load_unit(j, h);
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       unsigned vbase = 0;      // V units consumed before this step
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
       for (int j = 0; j < nsteps; ++j) {
-        const int kind = step_kind(p, j, qi);
+        const int kind = step_kind(gate_mode, j, qi);
         uint32_t prev = 0;     // gate tiles already assigned a V slot this step
         unsigned nunits = 0;   // V units of this step
         unsigned uidx[GT];
@@ -429,7 +435,6 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     const float sl2 = p.scale_log2;
     const float scale = p.scale;
     const float rescale_raw = p.rescale_raw;
-    const uint32_t xvote = xch_sm + s * C::XCH_TILE;  // u32 [2 parity][4 warps]
     const bool tr0 = BSFA_TRACE && tr_cta && r == 0;
     const uint32_t p_half = p_full + 16 * s;
 
@@ -454,17 +459,17 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
 
-      const int kind = CALIB ? kStepDynamic : step_kind(p, j, qi);
+      const int kind = CALIB ? kStepDynamic : step_kind(gate_mode, j, qi);
       if (!CALIB) {
-        if (j == qi && p.causal) {  // frontier step: key offset c vs row r inside block i
+        if (j == qi && causal) {  // frontier step: key offset c vs row r inside block i
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c > r) sv[c] = __float_as_uint(-INFINITY);
         }
-        if (!p.causal && (j + 1) * 128 > p.valid_len) {
+        if (!causal && (j + 1) * 128 > valid_len) {
 #pragma unroll
           for (int c = 0; c < 128; ++c)
-            if (j * 128 + c >= p.valid_len) sv[c] = __float_as_uint(-INFINITY);
+            if (j * 128 + c >= valid_len) sv[c] = __float_as_uint(-INFINITY);
         }
       }
       // row max per 64-key half (three-input FMNMX, four chains each)
@@ -487,7 +492,6 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         a1 = fmax3(a1, __uint_as_float(x[62]), __uint_as_float(x[63]));
         mh[hh] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
       }
-      if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();  // max done
       // gate-tile maxima: b_n = 64 -> the halves; b_n = 128 -> the whole row
       float mx[GT];
       if constexpr (GT == 2) {
@@ -520,14 +524,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         } else if (kind == kStepNone) {
           bits = 0;
         } else {
-          uint32_t wv = 0;
+          // OR over the tile's 128 rows in the barrier hardware (BAR.RED.OR)
+          bits = 0;
 #pragma unroll
-          for (int x = 0; x < GT; ++x) wv |= (__ballot_sync(0xffffffffu, mx[x] * scale > T) != 0u ? 1u : 0u) << x;
-          const uint32_t par = j & 1;
-          if (lane == 0) sts_u32(xvote + (par * 4 + wq) * 4, wv);
-          named_bar_sync(1 + s, 128);
-          const uint4 v4 = lds_u128(xvote + par * 16);
-          bits = v4.x | v4.y | v4.z | v4.w;
+          for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvVoted * 2 + s) * kTraceSteps + j] = clock64();
         if (r == 0) {
@@ -547,6 +547,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           }
         }
         if (kind == kStepDynamic) ++dn;
+        if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();  // lead post done
         if (bits == 0) {
           tc_fence_before();
           __syncwarp();
