@@ -9,6 +9,10 @@
 
 #include "../../include/bsfa_b200.h"
 #include "bsfa_kernel.cuh"
+#ifndef BSFA_GATE_STEP
+#define BSFA_GATE_STEP 0
+#endif
+#include "bsfa_kernel_gs.cuh"
 
 using namespace bsfa;
 
@@ -91,22 +95,54 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
   return BSFA_OK;
 }
 
+template <int D, int NQ, bool CALIB>
+int launch_gs(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+              cudaStream_t st) {
+  using C = GsCfg<D, NQ, CALIB>;
+  auto kern = bsfa_kernel_gs<D, NQ, CALIB>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  if (grid == 0) return BSFA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
+  return BSFA_OK;
+}
+
+// The 128-key-step kernel serves both gate widths (b_n = 64: two gate tiles
+// per step).  -DBSFA_GATE_STEP=1 builds the 64-key-step variant with a
+// double-buffered S ring instead (bsfa_kernel_gs.cuh; correct, tensor-bound,
+// but its 128x64x16 QK MMAs cost as much as 128x128x16 ones).
 // NQ = 2 query tiles (two q heads of one GQA group) per CTA when the group
-// size is even, else 1.
+// size is even.
 template <bool CALIB>
 int dispatch(int d, int b_n, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& p, int grid, cudaStream_t st) {
+#define BSFA_GS(D_, NQ_) \
+  if (d == D_ && b_n == 64 && nq == NQ_) return launch_gs<D_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
 #define BSFA_CASE(D_, BN_, NQ_) \
   if (d == D_ && b_n == BN_ && nq == NQ_) return launch<D_, 128 / BN_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
+#if BSFA_GATE_STEP
+  BSFA_GS(64, 1)
+  BSFA_GS(64, 2)
+  BSFA_GS(128, 1)
+  BSFA_GS(128, 2)
+#else
   BSFA_CASE(64, 64, 1)
   BSFA_CASE(64, 64, 2)
-  BSFA_CASE(64, 128, 1)
-  BSFA_CASE(64, 128, 2)
   BSFA_CASE(128, 64, 1)
   BSFA_CASE(128, 64, 2)
+#endif
+  BSFA_CASE(64, 128, 1)
+  BSFA_CASE(64, 128, 2)
   BSFA_CASE(128, 128, 1)
   BSFA_CASE(128, 128, 2)
 #undef BSFA_CASE
+#undef BSFA_GS
   return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
 }
 
@@ -162,8 +198,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   CUtensorMap tq, tk, tv;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b, 128,
-                       "k"))
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
+                       (BSFA_GATE_STEP && a->b_n == 64) ? 64 : 128, "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))
@@ -226,7 +262,9 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   const int d = a->head_dim, n = a->seq_len;
   CUtensorMap tq, tk;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, 1, a->q_stride_n, a->q_stride_h, 0, 128, "q")) return rc;
-  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0, 128, "k")) return rc;
+  if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0,
+                       (BSFA_GATE_STEP && a->b_n == 64) ? 64 : 128, "k"))
+    return rc;
 
   KernelParams p;
   memset(&p, 0, sizeof(p));

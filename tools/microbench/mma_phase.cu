@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* out, int reps) {
   uint8_t* sQ = base;             // 32 KB
   uint8_t* sK = base + 32768;     // 32 KB
   uint8_t* sV = base + 65536;     // 32 KB
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 98304);
+  const uint32_t bar = smem_u32(base + 98304);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(base + 98304 + 64);
   for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x3c003c00u;
   const int warp = threadIdx.x >> 5;
@@ -54,11 +54,21 @@ __global__ void __launch_bounds__(128, 1) k(long long* out, int reps) {
     umma_commit_w(bar);
     mbar_wait(bar, reps & 1);
     long long t6 = clock64();
+    // mode E: 64 back-to-back QK tiles at N=64 (8 MMAs each, K tile 64 rows)
+    {
+      constexpr uint32_t IQ64 = make_idesc_bf16(128, 64, 0, 0);
+      long long a0 = clock64();
+      for (int it = 0; it < 64; ++it) umma_qk_tile_w<128, 64>(tmem + 256 + (it & 3) * 64, dq, dk, IQ64);
+      umma_commit_w(bar);
+      mbar_wait(bar, (reps & 1) ^ 1);
+      long long a1 = clock64();
+      if (threadIdx.x == 0) out[7] = a1 - a0;
+    }
     // mode D: 64 back-to-back PV halves (4 MMAs each)
     for (int it = 0; it < 64; ++it) umma_pv64_w(tmem + (it & 1) * 128, tmem + 256, dv, IPV, 1);
     long long t7 = clock64();
     umma_commit_w(bar);
-    mbar_wait(bar, (reps & 1) ^ 1);
+    mbar_wait(bar, reps & 1);
     long long t8 = clock64();
     if (threadIdx.x == 0) { out[3] = t5 - t4; out[4] = t6 - t4; out[5] = t7 - t6; out[6] = t8 - t6; }
   }
@@ -73,6 +83,7 @@ int main() {
   k<<<1, 128, 100 * 1024>>>(d, 16);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[8]; cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
+  printf("64 QK tiles N=64: %lld cyc -> %.1f cyc/MMA (ideal 32)\n", h[7], h[7] / 512.0);
   printf("err=%s\n", cudaGetErrorString(e));
   printf("phase: issue 16 MMAs %lld cyc, issue->commit observed %lld cyc (ideal 1024)\n", h[0], h[1]);
   printf("single QK tile (8 MMAs) issue->observed %lld cyc (ideal 512)\n", h[2]);
