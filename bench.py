@@ -58,6 +58,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
+                    help="multi-GPU: batch = weak scaling (rank r owns batch element r); heads = strong scaling "
+                         "over kv-head groups of one batch-1 problem (configs[3])")
+    ap.add_argument("--gather", action="store_true",
+                    help="with --shard heads: all-gather O over NCCL inside every timed step")
     return ap.parse_args()
 
 
@@ -338,12 +343,31 @@ def main():
     k_level = costs.k_for_density(n, tiles, args.density)
     thr = calibrated_thresholds(cfg, tiles, k_level, dev)
 
-    q, k, v = make_inputs(cfg, rank, dev)  # rank r = batch element r (weak scaling)
-    plan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level, device=dev)
     stream = torch.cuda.current_stream(dev)
+    head_offset = 0
+    gather_buf = None
+    if args.shard == "heads" and world > 1:
+        # strong scaling: rank r owns kv heads [r*Hkv/W, (r+1)*Hkv/W) of one problem
+        from paper_2512_07011_b200.distributed import shard_heads
+        sh = shard_heads(hq, hkv, world, rank)
+        qf, kf, vf = make_inputs(cfg, 0, dev)
+        q = qf[:, sh.q_lo:sh.q_hi].contiguous()
+        k = kf[:, sh.kv_lo:sh.kv_hi].contiguous()
+        v = vf[:, sh.kv_lo:sh.kv_hi].contiguous()
+        del qf, kf, vf
+        hq, hkv, head_offset = sh.num_q, sh.num_kv, sh.q_lo
+        if args.gather:
+            gather_buf = torch.empty((world * hq, n, d), dtype=torch.bfloat16, device=dev)
+    else:
+        q, k, v = make_inputs(cfg, rank, dev)  # rank r = batch element r (weak scaling)
+    plan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level, head_offset=head_offset,
+                         device=dev)
 
     def step():
-        plan.run(q, k, v)
+        o = plan.run(q, k, v)
+        if gather_buf is not None:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gather_buf, o.view(hq, n, d))
 
     barrier(world)
     torch.cuda.synchronize()
@@ -412,12 +436,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": args.config, "batch_per_gpu": 1, "global_batch": world, **cfg,
+            "config": {"workload": args.config, "batch_per_gpu": 1,
+                       "global_batch": 1 if (args.shard == "heads" and world > 1) else world, **cfg,
                        "tiles": "128x64", "causal": True, "k_level": k_level,
                        "predicted_density": costs.predicted_density(n, tiles, k_level),
-                       "parallelism": f"kv-group/batch sharding x{world}, no collective",
+                       "parallelism": (f"kv-head-group sharding x{world}" + (", NCCL all-gather of O per step"
+                                       if gather_buf is not None else ", no collective"))
+                       if (args.shard == "heads" and world > 1) else f"batch sharding x{world}, no collective",
                        "l2": "inputs (Q/K/V 384 MiB at 32K) exceed the 126 MB L2; no explicit flush",
                        "thresholds": "calibrated on a separate synthetic sample (seed 1000)"},
             "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / vunits,
