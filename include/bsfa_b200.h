@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BSFA_ABI_VERSION 2
+#define BSFA_ABI_VERSION 3
 
 /* error codes */
 #define BSFA_OK 0
@@ -45,6 +45,8 @@ extern "C" {
 #define BSFA_GATE_THRESHOLD 0 /* ThresholdGate: keep iff tile max (scaled) > T   gates.py:59-78 */
 #define BSFA_GATE_DENSE 1     /* DenseGate: keep every reachable tile            gates.py:41-47 */
 #define BSFA_GATE_FRONTIER 2  /* FrontierOnlyGate: skip every off-frontier tile  gates.py:50-56 */
+#define BSFA_GATE_WINDOW 3    /* SlidingWindowGate(gate_window tokens)          gates.py:81-98  */
+#define BSFA_GATE_RUNMAX 4    /* RunningMaxGate(gate_lambda)                    gates.py:101-118 */
 
 /* counters written by bsfa_fwd (accumulated with atomics, caller zeroes) */
 #define BSFA_CNT_REACHABLE 0 /* reachable gate tiles (frontier included)        */
@@ -79,6 +81,8 @@ typedef struct bsfa_fwd_args {
   int causal;
   float scale; /* fp32(1/sqrt(original head_dim)) */
   int inject_fault;
+  int gate_window;   /* BSFA_GATE_WINDOW: trailing window w >= 0 (tokens) */
+  float gate_lambda; /* BSFA_GATE_RUNMAX: keep iff max_rows(local - running max) >= lambda */
 } bsfa_fwd_args;
 
 typedef struct bsfa_calib_args {

@@ -1,7 +1,8 @@
 """B200-native Block-Sparse FlashAttention (arXiv 2512.07011), sm_100a.
 
 Drop-in for the reference ``bsfa`` package's hot path: ``flash_forward`` with
-Threshold/Dense/FrontierOnly gates, ``calibrate`` / ``collect_block_maxima``,
+Threshold/Dense/FrontierOnly (and the paper's sliding-window / running-max
+baseline) gates, ``calibrate`` / ``collect_block_maxima``,
 and the ``ThresholdTensor`` file format -- executed by hand-written tcgen05 /
 TMA kernels behind the C ABI in ``include/bsfa_b200.h``.  ``attention`` is the
 batched GQA entry point on CUDA tensors.
@@ -12,8 +13,8 @@ from .errors import (BsfaError, ConfigurationError, DegenerateRowError, FormatEr
 from .tiling import (TileConfig, frontier_blocks, frontier_count, kernel_supports,
                      off_frontier_count)
 from .thresholds import ThresholdTensor, load_thresholds, save_thresholds, threshold_lookup
-from .gates import (DenseGate, FrontierOnlyGate, GateContext, ThresholdGate, dense_gate,
-                    frontier_only_gate, threshold_gate)
+from .gates import (DenseGate, FrontierOnlyGate, GateContext, RunningMaxGate, SlidingWindowGate,
+                    ThresholdGate, dense_gate, frontier_only_gate, threshold_gate)
 from .core import AttentionOutput, BlockMask, HeadInput
 from .trace import FRONTIER, KEPT, SKIPPED, UNREACHABLE, GateTrace
 from .attention import AttentionResult, BsfaPlan, attention, flash_forward, reference_scale

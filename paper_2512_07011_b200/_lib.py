@@ -16,7 +16,7 @@ from .errors import BsfaError
 LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 BSFA_OK = 0
 BSFA_ERR_INVALID = -1
@@ -26,6 +26,8 @@ BSFA_ERR_UNSUPPORTED = -3
 GATE_THRESHOLD = 0
 GATE_DENSE = 1
 GATE_FRONTIER = 2
+GATE_WINDOW = 3
+GATE_RUNMAX = 4
 
 CNT_REACHABLE = 0
 CNT_KEPT = 1
@@ -70,6 +72,8 @@ class FwdArgs(ctypes.Structure):
         ("causal", ctypes.c_int),
         ("scale", ctypes.c_float),
         ("inject_fault", ctypes.c_int),
+        ("gate_window", ctypes.c_int),
+        ("gate_lambda", ctypes.c_float),
     ]
 
 

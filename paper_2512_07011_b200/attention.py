@@ -35,7 +35,7 @@ import torch
 from . import _lib
 from .core import AttentionOutput, HeadInput
 from .errors import ConfigurationError, InvalidInputError, NumericError
-from .gates import GateContext, ThresholdGate, kernel_gate_mode
+from .gates import GateContext, ThresholdGate, gate_params, kernel_gate_mode
 from .thresholds import ThresholdTensor
 from .tiling import TileConfig, require_kernel_tiles
 from .trace import GateTrace
@@ -180,6 +180,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         a.causal = 1 if causal else 0
         a.scale = sc
         a.inject_fault = 1 if inject_fault else 0
+        a.gate_window, a.gate_lambda = gate_params(gate) if thr_dev is None else (0, 0.0)
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(_lib.load_library().bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
 
@@ -291,6 +292,7 @@ class BsfaPlan:
         a.causal = 1 if causal else 0
         a.scale = reference_scale(head_dim)
         a.inject_fault = 0
+        a.gate_window, a.gate_lambda = gate_params(gate) if self.thr is None else (0, 0.0)
         self.args = a
         self.lib = _lib.load_library()
 

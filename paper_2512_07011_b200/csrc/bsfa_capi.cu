@@ -187,7 +187,11 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
   if (a->valid_len < 1 || a->valid_len > a->seq_len) return fail(BSFA_ERR_INVALID, "bad valid_len %d", a->valid_len);
-  if (a->gate_mode < 0 || a->gate_mode > 2) return fail(BSFA_ERR_INVALID, "bad gate_mode %d", a->gate_mode);
+  if (a->gate_mode < 0 || a->gate_mode > 4) return fail(BSFA_ERR_INVALID, "bad gate_mode %d", a->gate_mode);
+  if (a->gate_mode == BSFA_GATE_WINDOW && a->gate_window < 0)
+    return fail(BSFA_ERR_INVALID, "window must be >= 0, got %d", a->gate_window);
+  if (BSFA_GATE_STEP && a->gate_mode > BSFA_GATE_FRONTIER)
+    return fail(BSFA_ERR_INVALID, "gate mode %d not built into the gate-step variant", a->gate_mode);
   if (a->gate_mode == BSFA_GATE_THRESHOLD && (!a->thresholds || a->thr_positions < 1))
     return fail(BSFA_ERR_INVALID, "threshold gate needs a [heads_q][positions] threshold array");
   if (!a->q || !a->k || !a->v || !a->o || !a->lse) return fail(BSFA_ERR_INVALID, "null tensor pointer");
@@ -223,6 +227,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.rescale_raw = 8.0f / p.scale_log2;
   p.inject_fault = a->inject_fault;
+  p.gate_window = a->gate_window;
+  p.gate_lambda = a->gate_lambda;
   p.thr = a->thresholds;
   p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
   p.o_sb = a->o_stride_b;

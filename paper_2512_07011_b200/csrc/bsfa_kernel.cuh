@@ -55,7 +55,7 @@
 
 namespace bsfa {
 
-enum : int { kGateThreshold = 0, kGateDense = 1, kGateFrontier = 2 };
+enum : int { kGateThreshold = 0, kGateDense = 1, kGateFrontier = 2, kGateWindow = 3, kGateRunMax = 4 };
 // static decision of a step (known to every role without the softmax)
 enum : int { kStepDynamic = 0, kStepAll = 1, kStepNone = 2 };
 
@@ -73,6 +73,8 @@ struct KernelParams {
   float scale_log2;
   float rescale_raw;  // lazy-rescale threshold in raw score units
   int inject_fault;
+  int gate_window;     // kGateWindow: trailing window in tokens (gates.py:81-98)
+  float gate_lambda;   // kGateRunMax: lambda (gates.py:101-118)
   const float* thr;
   __nv_bfloat16* o;
   long long o_sb, o_sh, o_sn;
@@ -151,11 +153,27 @@ struct KCfg {
   static_assert(CALIB || VS >= 2 * GT, "V ring must hold two steps");
 };
 
-// Static decision of step j (identical in every role).
-__device__ __forceinline__ int step_kind(int gate_mode, int j, int qi) {
-  if (j == qi || gate_mode == kGateDense) return kStepAll;  // frontier (tiling.py:50-60) / DenseGate
-  if (gate_mode == kGateFrontier) return kStepNone;          // FrontierOnlyGate
-  return kStepDynamic;
+// Statically known decision bits (bit x = gate tile x of the step) of step j,
+// or -1 when the step is decided by a vote over its scores.  Identical in
+// every role, so the V producer can prefetch static keeps without a vote.
+template <int GT>
+__device__ __forceinline__ int step_static_bits(int gate_mode, int window, int j, int qi) {
+  constexpr int kAll = (1 << GT) - 1;
+  if (j == qi || gate_mode == kGateDense) return kAll;  // frontier (tiling.py:50-60) / DenseGate
+  if (gate_mode == kGateFrontier) return 0;             // FrontierOnlyGate
+  if (gate_mode == kGateWindow) {
+    // SlidingWindowGate (gates.py:96-98): keep gate tile g iff its key range
+    // intersects [i*b_m - w, (i+1)*b_m)
+    constexpr int BN = 128 / GT;
+    int bits = 0;
+#pragma unroll
+    for (int x = 0; x < GT; ++x) {
+      const int gc = j * GT + x;
+      if ((gc + 1) * BN > qi * 128 - window && gc * BN < (qi + 1) * 128) bits |= 1 << x;
+    }
+    return bits;
+  }
+  return -1;  // ThresholdGate / RunningMaxGate: voted
 }
 
 template <int D, int GT, int NQ, bool CALIB>
@@ -164,7 +182,6 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
                 const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
   using C = KCfg<D, GT, NQ, CALIB>;
   constexpr int BN = C::BN, KS = C::KS, VS = C::VS, DQ = C::DQ;
-  constexpr uint32_t kAllBits = (1u << GT) - 1u;
 
   extern __shared__ uint8_t smem_raw[];
   // all shared-memory addresses are 32-bit shared-window offsets computed once
@@ -210,6 +227,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
   // off-frontier prefix only (calibration.py:110-113)
   const int nsteps = CALIB ? qi : (p.causal ? qi + 1 : p.num_steps);
   const int gate_mode = p.gate_mode;
+  const int window = p.gate_window;
   const bool causal = p.causal != 0;
   const int valid_len = p.valid_len;
   const bool tr_cta = BSFA_TRACE && p.trace && (int)blockIdx.x == p.trace_cta;
@@ -296,11 +314,12 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
           ++vcount;
         };
         for (int j = 0; j < nsteps; ++j) {
-          const int kind = step_kind(gate_mode, j, qi);
-          if (kind == kStepAll) {
+          const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
+          if (sb >= 0) {
 #pragma unroll
-            for (int h = 0; h < GT; ++h) load_unit(j, h);
-          } else if (kind == kStepDynamic) {
+            for (int h = 0; h < GT; ++h)
+              if ((sb >> h) & 1) load_unit(j, h);
+          } else {
             // query tile 0's keeps are fetched as soon as its vote is in; the
             // tiles only tile 1 keeps follow its vote (same order in the MMA warp)
             uint32_t prev = 0;
@@ -357,7 +376,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       unsigned vbase = 0;      // V units consumed before this step
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
       for (int j = 0; j < nsteps; ++j) {
-        const int kind = step_kind(gate_mode, j, qi);
+        const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
         uint32_t prev = 0;     // gate tiles already assigned a V slot this step
         unsigned nunits = 0;   // V units of this step
         unsigned uidx[GT];
@@ -373,11 +392,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
               p.trace[(kEvPSeen * 2 + s) * kTraceSteps + j] = clock64();
             tc_fence_after();
             if constexpr (!CALIB) {
-              if (hh == 0) {
-                if (kind == kStepAll) bits = kAllBits;
-                else if (kind == kStepNone) bits = 0;
-                else bits = lds_u32(decm_sm + s * 4);
-              }
+              if (hh == 0) bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + s * 4);
               const int x = GT == 2 ? hh : 0;  // gate tile of this half
               if ((bits >> x) & 1u) {
                 if (hh == 0 || GT == 2) {
@@ -444,6 +459,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       T = p.thr[(long long)hq * p.thr_positions + pos];
     }
 
+    const float lam = p.gate_lambda;
+    float m_true = -INFINITY;  // exact running row max (RunningMaxGate), raw units
     float m_ref = -INFINITY;  // raw (unscaled) reference max of this row over its kept tiles
     float l_sum = 0.f;        // row sum relative to m_ref
     bool o_valid = false;     // tile-uniform: O_s holds data
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
 
-      const int kind = CALIB ? kStepDynamic : step_kind(gate_mode, j, qi);
+      const int sb = CALIB ? -1 : step_static_bits<GT>(gate_mode, window, j, qi);
       if (!CALIB) {
         if (j == qi && causal) {  // frontier step: key offset c vs row r inside block i
 #pragma unroll
@@ -517,21 +534,38 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
         }
         continue;
       } else {
-        // ---- gate: OR over the tile's 128 rows of (rowmax * scale > T)
+        // ---- gate decision; votes are OR-reduced over the tile's 128 rows in the
+        //      barrier hardware (BAR.RED.OR)
         uint32_t bits;
-        if (kind == kStepAll) {
-          bits = kAllBits;
-        } else if (kind == kStepNone) {
-          bits = 0;
-        } else {
-          // OR over the tile's 128 rows in the barrier hardware (BAR.RED.OR)
+        if (sb >= 0) {
+          bits = uint32_t(sb);
+        } else if (gate_mode == kGateThreshold) {
+          // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
           bits = 0;
 #pragma unroll
           for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
+        } else {
+          // RunningMaxGate: keep iff max over rows of (local row max - running
+          // row max) >= lambda, judged before the tile is merged; tiles in key
+          // order, so gate tile 1 sees tile 0 merged if it was kept
+          // (gates.py:101-118; -inf running max gives +inf: keep)
+          bits = 0;
+          float mrun = m_true;
+#pragma unroll
+          for (int x = 0; x < GT; ++x) {
+            const uint32_t k = named_bar_red_or(1 + s, 128, (mx[x] - mrun) * scale >= lam ? 1u : 0u);
+            bits |= k << x;
+            if (k) mrun = fmaxf(mrun, mx[x]);
+          }
+        }
+        if (gate_mode == kGateRunMax) {
+#pragma unroll
+          for (int x = 0; x < GT; ++x)
+            if ((bits >> x) & 1u) m_true = fmaxf(m_true, mx[x]);
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvVoted * 2 + s) * kTraceSteps + j] = clock64();
         if (r == 0) {
-          if (kind == kStepDynamic) {
+          if (sb < 0) {
             const int di = int(dn % DQ);
             mbar_wait((dec_empty + 8 * (s * DQ + di)), ((dn / DQ) & 1) ^ 1);
             sts_u32(dec_sm + (s * DQ + di) * 4, bits);
@@ -546,8 +580,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
               drow[j * GT + x] = j == qi ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
           }
         }
-        if (kind == kStepDynamic) ++dn;
-        if (tr0 && j < kTraceSteps) p.trace[(kEvLdDone * 2 + s) * kTraceSteps + j] = clock64();  // lead post done
+        if (sb < 0) ++dn;
         if (bits == 0) {
           tc_fence_before();
           __syncwarp();

@@ -327,6 +327,69 @@ def test_unsupported_gate_and_tiles_refused(bsfa):
         bsfa.flash_forward(inp, bsfa.TileConfig(64, 64), bsfa.dense_gate())
 
 
+# ------------------------------------------------------------------ paper baseline gates
+@pytest.mark.parametrize("n,d,b_n,window", [(1024, 64, 64, 0), (1024, 128, 64, 300), (1000, 128, 128, 256),
+                                            (2048, 128, 64, 1024)])
+def test_sliding_window_gate(bsfa, n, d, b_n, window):
+    """SlidingWindowGate (gates.py:81-98): static decisions must match exactly."""
+    rng = np.random.default_rng(n + window)
+    q, k, v = (orc.round_bf16(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3))
+    tiles = bsfa.TileConfig(128, b_n)
+    out, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.SlidingWindowGate(window))
+    o_ref, lse_ref, dec_ref = orc.flash_forward(q, k, v, True, 128, b_n, orc.sliding_window_gate(window, 128, b_n))
+    assert np.array_equal(trace.decisions, dec_ref)
+    assert np.abs(out.o - o_ref).max() <= ATOL
+    assert np.abs(out.logsumexp - lse_ref).max() <= ATOL
+
+
+@pytest.mark.parametrize("lam,b_n", [(-0.5, 64), (0.5, 64), (1.0, 64), (0.5, 128), (1.5, 128)])
+def test_running_max_gate(bsfa, lam, b_n):
+    """RunningMaxGate (gates.py:101-118): decisions equal the oracle's except
+    tiles whose max (local - running) difference lies within EPS of lambda;
+    output parity by replaying the GPU decisions in the oracle engine."""
+    rng = np.random.default_rng(int(10 * lam) + b_n)
+    n, d = 2048, 128
+    q, k, v = (orc.round_bf16(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(3))
+    tiles = bsfa.TileConfig(128, b_n)
+    out, trace = bsfa.flash_forward(bsfa.HeadInput(q, k, v), tiles, bsfa.RunningMaxGate(lam))
+    diffs = {}
+
+    def recording_gate(s, i, j, m):
+        with np.errstate(invalid="ignore"):
+            dmax = float((s.max(axis=1) - m).max())
+        diffs[(i, j)] = dmax
+        return dmax >= lam
+
+    _, _, dec_ref = orc.flash_forward(q, k, v, True, 128, b_n, recording_gate)
+    bad = [(i, j) for (i, j) in zip(*np.nonzero(trace.decisions != dec_ref))
+           if not abs(diffs.get((int(i), int(j)), np.inf) - lam) <= EPS]
+    assert not bad, bad[:5]
+    dec = trace.decisions
+    if lam >= 0:  # the gate actually prunes at these settings
+        assert (dec == orc.SKIPPED).any() and (dec == orc.KEPT).any()
+    o_ref, _, _ = orc.flash_forward(q, k, v, True, 128, b_n, orc.replay_gate(dec))
+    assert np.abs(out.o - o_ref).max() <= ATOL
+
+
+def test_window_gate_in_batched_gqa_launch(bsfa):
+    """Static gate through the batched API: V fetches only for window tiles."""
+    rng = np.random.default_rng(5)
+    B, hq, hkv, n, d = 1, 4, 2, 2048, 128
+    q = _dev(rng.standard_normal((B, hq, n, d)).astype(np.float32))
+    k = _dev(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    v = _dev(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    res = bsfa.attention(q, k, v, gate=bsfa.SlidingWindowGate(256), return_trace=True)
+    dec = res.decisions.cpu().numpy()
+    c = res.counters.cpu().numpy()
+    kept = dec >= 2
+    assert c[2] == np.count_nonzero(kept[:, 0::2] | kept[:, 1::2])
+    # every query block keeps exactly its frontier plus the tiles meeting the window
+    for i in range(n // 128):
+        row = dec[0, 0, i]
+        want = [j for j in range(2 * i) if (j + 1) * 64 > i * 128 - 256]
+        assert list(np.nonzero(row == orc.KEPT)[0]) == want
+
+
 # ------------------------------------------------------------------ calibration
 def test_calibration_matches_reference_golden(bsfa):
     c = load_golden("calib")
