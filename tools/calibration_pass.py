@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 
 import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import costs  # noqa: E402
+from paper_2512_07011_b200.report import measured_density, save_traces, traces_from_decisions, write_report  # noqa: E402
 from paper_2512_07011_b200.workloads import model_dump_layer  # noqa: E402
 from oracle import bsfa_oracle as orc  # noqa: E402
 
@@ -44,6 +45,8 @@ def main():
     ap.add_argument("--seq", type=int, default=32768)
     ap.add_argument("--samples", type=int, default=2)
     ap.add_argument("--oracle-heads", type=int, default=2)
+    ap.add_argument("--traces", default=None, help="write the evaluation decisions (reference npz trace format)")
+    ap.add_argument("--report", default=None, help="write a reference schema-1 run report (JSON)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -81,6 +84,7 @@ def main():
     # ---- 2. held-out evaluation, dense vs BSFA per layer
     rows = []
     eval_sample = 1000
+    traces = []
     for layer in range(L):
         q, k, v = model_dump_layer(eval_sample, layer, HQ, HKV, n, D, device=dev)
         q, k, v = q[None], k[None], v[None]
@@ -88,11 +92,14 @@ def main():
         e[0].record()
         rd = bsfa.attention(q, k, v, tiles=tiles)
         e[1].record()
-        rb = bsfa.attention(q, k, v, thresholds=thr, layer=layer, k_level=k50, tiles=tiles)
+        rb = bsfa.attention(q, k, v, thresholds=thr, layer=layer, k_level=k50, tiles=tiles,
+                            return_trace=args.traces is not None or args.report is not None)
         e[2].record()
         torch.cuda.synchronize()
         c = rb.counters.cpu().numpy()
         dev_max = float((rb.o.float() - rd.o.float()).abs().max())
+        if rb.decisions is not None:
+            traces.extend(traces_from_decisions(rb.decisions, tiles, causal=True, layer=layer))
         rows.append({"layer": layer, "density": float(c[1] / c[0]), "dense_ms": e[0].elapsed_time(e[1]),
                      "bsfa_ms": e[1].elapsed_time(e[2]), "max_abs_bsfa_vs_dense": dev_max})
     dens = np.array([r["density"] for r in rows])
@@ -103,6 +110,23 @@ def main():
                       "bsfa_ms_total": sum(r["bsfa_ms"] for r in rows),
                       "speedup": sum(r["dense_ms"] for r in rows) / sum(r["bsfa_ms"] for r in rows),
                       "per_layer": rows}), flush=True)
+
+    if args.traces:
+        save_traces(args.traces, [traces], tiles, causal=True)
+    if args.report:
+        mean, std = measured_density([traces])
+        bsfa_ms = np.array([r["bsfa_ms"] for r in rows])
+        cc = costs.tile_counts(n, tiles)
+        per_tile = 2 * 128 * 64 * D
+        write_report(args.report,
+                     {"n": n, "d": D, "layers": L, "heads": HQ, "bm": 128, "bn": 64, "gate": "threshold",
+                      "params": {"k": k50, "device": "B200 sm_100a", "heads_kv": HKV}},
+                     {"mean_ms": float(bsfa_ms.mean()), "std_ms": float(bsfa_ms.std()), "repeats": L},
+                     {"qk_flops": per_tile * cc[0] * HQ, "pv_flops": per_tile * cc[0] * mean * HQ,
+                      "softmax_ops": 128 * 64 * cc[0] * mean * HQ, "v_traffic": 64 * D * cc[0] * mean * HQ,
+                      "k_traffic": 64 * D * cc[0] * HQ, "gate_overhead_ops": (128 * 64 + 1) * (cc[0] - cc[1]) * HQ},
+                     {"predicted": costs.predicted_density(n, tiles, k50), "measured_mean": mean,
+                      "measured_std": std}, None)
 
     # ---- 3. oracle spot checks on sampled (layer, head)
     rng = np.random.default_rng(7)
