@@ -77,11 +77,17 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
+// threads per softmax row of the forward kernel (1: 128 keys per thread, 2: 64)
+#ifndef BSFA_TPR
+#define BSFA_TPR 1
+#endif
+
 template <int D, int GT, int NQ, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  using C = KCfg<D, GT, NQ, CALIB>;
-  auto kern = bsfa_kernel<D, GT, NQ, CALIB>;
+  constexpr int TPR = CALIB ? 1 : BSFA_TPR;
+  using C = KCfg<D, GT, NQ, CALIB, TPR>;
+  auto kern = bsfa_kernel<D, GT, NQ, CALIB, TPR>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);

@@ -100,7 +100,7 @@ struct KernelParams {
 constexpr int kTraceSteps = 2048;
 enum : int { kEvSReady = 0, kEvVoted = 1, kEvPDone = 2, kEvPSeen = 3, kEvVReady = 4, kEvIssued = 5, kEvLdDone = 6, kEvExpDone = 7 };
 
-template <int D, int GT, int NQ, bool CALIB>
+template <int D, int GT, int NQ, bool CALIB, int TPR = 1>
 struct KCfg {
   static constexpr int BN = 128 / GT;        // gate tile width (reference b_n)
   static constexpr int NCH = D / 64;         // 128-byte swizzle atoms along head_dim
@@ -122,7 +122,9 @@ struct KCfg {
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
   static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 4 * NQ + 2 * NQ * DQ;
   // per query tile: per-warp gate votes u32 [2 parity][4 warps]
-  static constexpr int XCH_TILE = 2 * 4 * 4;
+  // per query tile (TPR = 2): half-row maxima f32 [2 parity][2 halves][128],
+  // then the epilogue row sums f32 [2 halves][128]
+  static constexpr int XCH_TILE = TPR == 2 ? (2 * 2 * 128 + 2 * 128) * 4 : 2 * 4 * 4;
   static constexpr int OFF_XCH = (OFF_BAR + NUM_BARS * 8 + 15) / 16 * 16;  // 16-B aligned: votes read as v4
   static constexpr int OFF_DEC = OFF_XCH + NQ * XCH_TILE;   // u32 [NQ][DQ] decision ring (V producer)
   static constexpr int OFF_DECM = OFF_DEC + NQ * DQ * 4;    // u32 [NQ] decision of the current step (MMA)
@@ -135,16 +137,22 @@ struct KCfg {
   static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
   // one thread per row: warpgroup s is query tile s; the last warpgroup holds
   // the K producer, the MMA issuer, the V producer and one idle warp
-  static constexpr int SOFTMAX_WARPS = 4 * NQ;
+  // TPR threads per row: warpgroup s*TPR + h owns key half h of query tile s
+  static constexpr int SOFTMAX_WARPS = 4 * NQ * TPR;
   static constexpr int KPROD_WARP = SOFTMAX_WARPS;
   static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static constexpr int VPROD_WARP = SOFTMAX_WARPS + 2;
   static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 4) * 32;
   // register split (setmaxnreg): softmax warps hold a 128-column score row,
   // its exponentials and the packed P row
-  static constexpr int REG_OTHER = 56;
-  static constexpr int REG_SOFT_MAX = (65536 - 128 * REG_OTHER) / (SOFTMAX_WARPS * 32) / 8 * 8;
+  // The setmaxnreg pool is what the CTA was launched with: NUM_THREADS x the
+  // launch-bound register count (65536 / NUM_THREADS, multiple of 8, <= 255).
+  // Growing the softmax warps beyond pool - 128 x REG_OTHER would block forever.
+  static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8 > 248 ? 248 : (65536 / NUM_THREADS) / 8 * 8;
+  static constexpr int REG_OTHER = TPR == 2 ? 32 : 56;
+  static constexpr int REG_SOFT_MAX = (NUM_THREADS * REG_LAUNCH - 128 * REG_OTHER) / (SOFTMAX_WARPS * 32) / 8 * 8;
   static constexpr int REG_SOFT = REG_SOFT_MAX > 248 ? 248 : REG_SOFT_MAX;
+  static_assert(REG_SOFT >= REG_LAUNCH && REG_OTHER <= REG_LAUNCH, "register split");
   static constexpr bool SPLIT_REGS = true;
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
   static_assert(NQ == 1 || NQ == 2, "one or two query tiles per CTA");
@@ -176,11 +184,12 @@ __device__ __forceinline__ int step_static_bits(int gate_mode, int window, int j
   return -1;  // ThresholdGate / RunningMaxGate: voted
 }
 
-template <int D, int GT, int NQ, bool CALIB>
-__global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
+template <int D, int GT, int NQ, bool CALIB, int TPR = 1>
+__global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     bsfa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = KCfg<D, GT, NQ, CALIB>;
+  using C = KCfg<D, GT, NQ, CALIB, TPR>;
+  static_assert(TPR == 1 || (TPR == 2 && !CALIB), "two threads per row: forward only");
   constexpr int BN = C::BN, KS = C::KS, VS = C::VS, DQ = C::DQ;
 
   extern __shared__ uint8_t smem_raw[];
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init((s_full + 8 * (s)), 1);
-      mbar_init((p_full + 8 * (2 * s)), 4);  // the 4 softmax warps of query tile s
+      mbar_init((p_full + 8 * (2 * s)), 4);  // the 4 softmax warps of query tile s (of half h, TPR = 2)
       mbar_init((p_full + 8 * (2 * s + 1)), 4);
       mbar_init((o_full + 8 * (s)), 1);
     }
@@ -432,6 +441,273 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB>::NUM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
     return;
+  } else if (TPR == 2 && warp < C::SOFTMAX_WARPS) {
+    if constexpr (TPR == 2) {
+      setmaxnreg_inc<C::REG_SOFT>();
+      // ======================= softmax, two threads per row (TPR = 2) ============
+      // Thread (s, h, r) owns row r of query tile s over the 64 keys [64h, 64h+64)
+      // of every step (gate tile h at b_n = 64, half of the gate tile at 128).
+      // The two threads of a row exchange half-row maxima at the vote barrier,
+      // so both keep the same running max; each keeps its half's row sum.
+      const int s = warp >> 3;
+      const int h = (warp >> 2) & 1;
+      const int wq = warp & 3;
+      const int r = wq * 32 + lane;
+      const int hq = hq0 + s;
+      const uint32_t lane_off = uint32_t(wq * 32) << 16;
+      const uint32_t s_row = tmem + lane_off + C::S_COL + s * 128;
+      const uint32_t o_row = tmem + lane_off + C::O_COL + s * D;
+      const float sl2 = p.scale_log2;
+      const float scale = p.scale;
+      const float rescale_raw = p.rescale_raw;
+      const float lam = p.gate_lambda;
+      const uint32_t xmax = xch_sm + s * C::XCH_TILE;  // f32 [2 par][2 h][128]
+      const uint32_t xfin = xmax + 2 * 2 * 128 * 4;    // f32 [2 h][128]
+      const bool lead = h == 0 && r == 0;
+      const bool tr0 = BSFA_TRACE && tr_cta && lead;
+      const uint32_t my_bit = GT == 2 ? (1u << h) : 1u;
+      const uint32_t other_bit = GT == 2 ? (1u << (h ^ 1)) : 1u;
+      const uint32_t p_mine = p_full + 16 * s + 8 * h;
+
+      float T = 0.f;
+      if (gate_mode == kGateThreshold) {
+        const int pos = qi < p.thr_positions - 1 ? qi : p.thr_positions - 1;
+        T = p.thr[(long long)hq * p.thr_positions + pos];
+      }
+      float m_true = -INFINITY;
+      float m_ref = -INFINITY;
+      float l_sum = 0.f;
+      bool o_valid = false;
+      unsigned dn = 0;
+      unsigned long long kept_tiles = 0;
+
+      for (int j = 0; j < nsteps; ++j) {
+        mbar_wait((s_full + 8 * (s)), j & 1);
+        if (tr0 && j < kTraceSteps) p.trace[(kEvSReady * 2 + s) * kTraceSteps + j] = clock64();
+        tc_fence_after();
+        uint32_t sv[64];
+        tmem_ld32(s_row + h * 64, &sv[0]);
+        tmem_ld32(s_row + h * 64 + 32, &sv[32]);
+        tmem_wait_ld();
+        const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
+        if (j == qi && causal) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (h * 64 + c > r) sv[c] = __float_as_uint(-INFINITY);
+        }
+        if (!causal && (j + 1) * 128 > valid_len) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (j * 128 + h * 64 + c >= valid_len) sv[c] = __float_as_uint(-INFINITY);
+        }
+        float mh;
+        {
+          float a0 = fmax3(__uint_as_float(sv[0]), __uint_as_float(sv[1]), __uint_as_float(sv[2]));
+          float a1 = fmax3(__uint_as_float(sv[3]), __uint_as_float(sv[4]), __uint_as_float(sv[5]));
+          float a2 = fmax3(__uint_as_float(sv[6]), __uint_as_float(sv[7]), __uint_as_float(sv[8]));
+          float a3 = fmax3(__uint_as_float(sv[9]), __uint_as_float(sv[10]), __uint_as_float(sv[11]));
+          float a4 = fmax3(__uint_as_float(sv[12]), __uint_as_float(sv[13]), __uint_as_float(sv[14]));
+          float a5 = fmax3(__uint_as_float(sv[15]), __uint_as_float(sv[16]), __uint_as_float(sv[17]));
+#pragma unroll
+          for (int c = 18; c < 60; c += 12) {
+            a0 = fmax3(a0, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]));
+            a1 = fmax3(a1, __uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3]));
+            a2 = fmax3(a2, __uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5]));
+            a3 = fmax3(a3, __uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7]));
+            a4 = fmax3(a4, __uint_as_float(sv[c + 8]), __uint_as_float(sv[c + 9]));
+            a5 = fmax3(a5, __uint_as_float(sv[c + 10]), __uint_as_float(sv[c + 11]));
+          }
+          a0 = fmax3(a0, __uint_as_float(sv[54]), __uint_as_float(sv[55]));
+          a1 = fmax3(a1, __uint_as_float(sv[56]), __uint_as_float(sv[57]));
+          a2 = fmax3(a2, __uint_as_float(sv[58]), __uint_as_float(sv[59]));
+          a3 = fmax3(a3, __uint_as_float(sv[60]), __uint_as_float(sv[61]));
+          a4 = fmax3(a4, __uint_as_float(sv[62]), __uint_as_float(sv[63]));
+          mh = fmax3(fmax3(a0, a1, a2), fmax3(a3, a4, a5), -INFINITY);
+        }
+        // ---- exchange half-row maxima and vote, one barrier round (256 threads)
+        const uint32_t par = j & 1;
+        float mo = -INFINITY;
+        uint32_t bits;
+        if (sb == 0) {
+          bits = 0;  // FrontierOnlyGate / window-excluded step: nobody needs maxima
+        } else {
+          sts_f32(xmax + ((par * 2 + h) * 128 + r) * 4, mh);
+          if (sb > 0) {
+            named_bar_sync(1 + s, 256);
+            bits = uint32_t(sb);
+          } else if (gate_mode == kGateThreshold) {
+            if constexpr (GT == 2) {
+              bits = named_bar_red_or(1 + s, 256, (h == 0 && mh * scale > T) ? 1u : 0u);
+              bits |= named_bar_red_or(1 + s, 256, (h == 1 && mh * scale > T) ? 1u : 0u) << 1;
+            } else {
+              bits = named_bar_red_or(1 + s, 256, mh * scale > T ? 1u : 0u);
+            }
+          } else {
+            // RunningMaxGate, gate tiles in key order (gates.py:101-118)
+            if constexpr (GT == 2) {
+              const uint32_t k0 = named_bar_red_or(1 + s, 256, (h == 0 && (mh - m_true) * scale >= lam) ? 1u : 0u);
+              const float m_half0 = lds_f32(xmax + ((par * 2 + 0) * 128 + r) * 4);
+              const float mrun = k0 ? fmaxf(m_true, m_half0) : m_true;
+              const uint32_t k1 = named_bar_red_or(1 + s, 256, (h == 1 && (mh - mrun) * scale >= lam) ? 1u : 0u);
+              bits = k0 | (k1 << 1);
+            } else {
+              const float mfull = fmaxf(mh, lds_f32(xmax + ((par * 2 + (h ^ 1)) * 128 + r) * 4));
+              bits = named_bar_red_or(1 + s, 256, (mfull - m_true) * scale >= lam ? 1u : 0u);
+            }
+          }
+          mo = lds_f32(xmax + ((par * 2 + (h ^ 1)) * 128 + r) * 4);
+        }
+        if (tr0 && j < kTraceSteps) p.trace[(kEvVoted * 2 + s) * kTraceSteps + j] = clock64();
+        const bool mine = (bits & my_bit) != 0;
+        const bool other = (bits & other_bit) != 0;
+        if (gate_mode == kGateRunMax) {
+          if (mine) m_true = fmaxf(m_true, mh);
+          if (other) m_true = fmaxf(m_true, mo);
+        }
+        if (lead) {
+          if (sb < 0) {
+            const int di = int(dn % DQ);
+            mbar_wait((dec_empty + 8 * (s * DQ + di)), ((dn / DQ) & 1) ^ 1);
+            sts_u32(dec_sm + (s * DQ + di) * 4, bits);
+            mbar_arrive((dec_full + 8 * (s * DQ + di)));
+          }
+          sts_u32(decm_sm + s * 4, bits);
+        }
+        if (sb < 0) ++dn;
+        if (bits == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_mine);
+          if (lead && p.decisions) {
+            int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi) * p.gate_cols;
+#pragma unroll
+            for (int x = 0; x < GT; ++x) drow[j * GT + x] = int8_t(1);
+          }
+          continue;
+        }
+        // running max over the kept halves (identical in both threads of the row)
+        const float m_step = fmaxf(mine ? mh : -INFINITY, other ? mo : -INFINITY);
+        const float m_new = fmaxf(m_ref, m_step);
+        float alpha = 1.f;
+        bool rescale = false;
+        if (!o_valid) {
+          m_ref = m_new;
+        } else if (m_new > m_ref + rescale_raw) {
+          alpha = ex2_approx((m_ref - m_new) * sl2);
+          m_ref = m_new;
+          rescale = true;
+        }
+        const bool kept_h = ((bits >> (GT == 2 ? h : 0)) & 1u) != 0;
+        float psum = 0.f;
+        if (kept_h) {
+          const float neg = (m_ref == -INFINITY) ? 0.f : -m_ref * sl2;
+          const uint64_t sl2x2 = f2_pack(sl2, sl2);
+          const uint64_t negx2 = f2_pack(neg, neg);
+          uint64_t acc0 = 0, acc1 = 0;
+#pragma unroll
+          for (int cb = 0; cb < 64; cb += 32) {  // two 32-key chunks: 16 packed registers live at a time
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = cb; c < cb + 32; c += 4) {
+              const uint64_t x0 = ffma2(f2_pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2x2, negx2);
+              const uint64_t x1 =
+                  ffma2(f2_pack(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), sl2x2, negx2);
+              const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
+              float p2, p3;
+              if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
+                const uint64_t x1d = BSFA_EXP_CHAIN ? ffma2(f2_pack(p0, p1), 0ull, x1) : x1;
+                const uint64_t e1 = exp2_poly_x2(x1d);
+                p2 = f2_lo(e1);
+                p3 = f2_hi(e1);
+              } else {
+                p2 = ex2_approx(f2_lo(x1));
+                p3 = ex2_approx(f2_hi(x1));
+              }
+              acc0 = fadd2(acc0, f2_pack(p0, p1));
+              acc1 = fadd2(acc1, f2_pack(p2, p3));
+              pk[(c - cb) / 2] = pack_bf16x2(p0, p1);
+              pk[(c - cb) / 2 + 1] = pack_bf16x2(p2, p3);
+            }
+            tmem_st16(s_row + h * 32 + cb / 2, pk);
+          }
+          const uint64_t acc = fadd2(acc0, acc1);
+          psum = f2_lo(acc) + f2_hi(acc);
+        }
+        // the half-0 threads rescale the whole O row before releasing half 0 (after
+        // their exponentials, when the score registers are free)
+        // (PV of half 1 is issued after PV of half 0, so it follows the rescale)
+        if (h == 0 && __any_sync(0xffffffffu, rescale)) {
+          const uint64_t ax2 = f2_pack(alpha, alpha);
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t ov[32];
+            tmem_ld32(o_row + c, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const uint64_t t = fmul2(f2_pack(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])), ax2);
+              ov[e] = __float_as_uint(f2_lo(t));
+              ov[e + 1] = __float_as_uint(f2_hi(t));
+            }
+            tmem_st32(o_row + c, ov);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_mine);
+        if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
+        l_sum = l_sum * alpha + psum;
+        if (lead) {
+          kept_tiles += __popc(bits);
+          if (p.decisions) {
+            int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi) * p.gate_cols;
+#pragma unroll
+            for (int x = 0; x < GT; ++x)
+              drow[j * GT + x] = j == qi ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+          }
+        }
+        o_valid = true;
+      }
+
+      // ---- epilogue: O = O~ / (l_0 + l_1), lse = m * scale + ln l
+      sts_f32(xfin + (h * 128 + r) * 4, l_sum);
+      mbar_wait((o_full + 8 * (s)), 0);
+      tc_fence_after();
+      named_bar_sync(3 + s, 256);
+      const float l_row = l_sum + lds_f32(xfin + ((h ^ 1) * 128 + r) * 4);
+      const float inv_l = 1.f / l_row;
+      bool bad = !(l_row > 0.f);
+      const int row = qi * 128 + r;
+      __nv_bfloat16* orow =
+          p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + h * (D / 2);
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 32) {
+        uint32_t ov[32];
+        tmem_ld32(o_row + h * (D / 2) + c, ov);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float a0 = __uint_as_float(ov[e]) * inv_l, a1 = __uint_as_float(ov[e + 1]) * inv_l;
+          if (p.inject_fault && qi == 0 && r == 0 && s == 0 && h == 0 && c == 0 && e == 0) a0 += 1.0f;
+          bad |= !isfinite(a0) || !isfinite(a1);
+          pk[e / 2] = pack_bf16x2(a0, a1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      }
+      if (h == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_row);
+      if (bad && p.status) atomicOr(p.status, 1);
+      if (lead && p.counters) {
+        atomicAdd(&p.counters[0], (unsigned long long)nsteps * GT);
+        atomicAdd(&p.counters[1], kept_tiles);
+      }
+      tc_fence_before();
+      named_bar_arrive(15, C::NUM_THREADS);
+      return;
+    }
   } else if (warp < C::SOFTMAX_WARPS) {
     if constexpr (C::SPLIT_REGS) setmaxnreg_inc<C::REG_SOFT>();
     // ======================= softmax group s (query tile s) =======================

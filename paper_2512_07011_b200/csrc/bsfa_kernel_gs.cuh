@@ -56,8 +56,9 @@ struct GsCfg {
   static constexpr int MMA_WARP = SOFTMAX_WARPS + 1;
   static constexpr int VPROD_WARP = SOFTMAX_WARPS + 2;
   static constexpr int NUM_THREADS = (SOFTMAX_WARPS + 4) * 32;
+  static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8 > 248 ? 248 : (65536 / NUM_THREADS) / 8 * 8;
   static constexpr int REG_OTHER = 56;
-  static constexpr int REG_SOFT_MAX = (65536 - 128 * REG_OTHER) / (SOFTMAX_WARPS * 32) / 8 * 8;
+  static constexpr int REG_SOFT_MAX = (NUM_THREADS * REG_LAUNCH - 128 * REG_OTHER) / (SOFTMAX_WARPS * 32) / 8 * 8;
   static constexpr int REG_SOFT = REG_SOFT_MAX > 248 ? 248 : REG_SOFT_MAX;
   static_assert(NQ == 1 || NQ == 2, "one or two query tiles per CTA");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
