@@ -107,8 +107,14 @@ struct KCfg {
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = 128 * D * 2;  // one 128-key step
   static constexpr int V_UNIT = BN * D * 2;   // one gate tile of V
-  static constexpr int KS = D == 128 ? 2 : 3;
-  static constexpr int VS = CALIB ? 0 : (D == 128 ? 81920 : 65536) / V_UNIT;
+#ifndef BSFA_K_STAGES
+#define BSFA_K_STAGES 3
+#endif
+#ifndef BSFA_V_BYTES
+#define BSFA_V_BYTES 65536
+#endif
+  static constexpr int KS = D == 128 ? BSFA_K_STAGES : 3;
+  static constexpr int VS = CALIB ? 0 : (D == 128 ? BSFA_V_BYTES : 65536) / V_UNIT;
 #ifndef BSFA_DQ
 #define BSFA_DQ 4
 #endif
