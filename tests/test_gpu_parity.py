@@ -506,3 +506,30 @@ def test_online_rescale_path(bsfa, d):
         o_ref, lse_ref, _ = orc.flash_forward(q, k, v, True, 128, 64, orc.replay_gate(trace.decisions))
         assert np.abs(out.o - o_ref).max() <= ATOL, gate
         np.testing.assert_allclose(out.logsumexp, lse_ref, atol=1e-2)
+
+
+@pytest.mark.parametrize("B,hq,hkv,chunks", [(1, 8, 4, 4), (2, 8, 4, 2), (1, 4, 4, 4), (2, 6, 2, 1)])
+def test_plan_run_host_matches_device_run(bsfa, B, hq, hkv, chunks):
+    """The pipelined host path (per kv-head group H2D | kernel | D2H) is the device launch, bit for bit."""
+    rng = np.random.default_rng(B * 100 + hq * 10 + chunks)
+    n, d = 2048, 128
+    q = torch.from_numpy(rng.standard_normal((B, hq, n, d)).astype(np.float32)).to(torch.bfloat16)
+    k = torch.from_numpy(rng.standard_normal((B, hkv, n, d)).astype(np.float32)).to(torch.bfloat16)
+    v = torch.from_numpy(rng.standard_normal((B, hkv, n, d)).astype(np.float32)).to(torch.bfloat16)
+    vals = (3.6 + 0.2 * rng.standard_normal((1, 1, hq, n // 128))).astype(np.float32)
+    t = bsfa.ThresholdTensor(values=vals, k_levels=(3,), n_max=n, b_m=128, b_n=64)
+    plan = bsfa.BsfaPlan(B, hq, hkv, n, d, thresholds=t, k_level=3, return_trace=True)
+    o_dev = plan.run(q.cuda(), k.cuda(), v.cuda()).clone()
+    lse_dev, dec_dev, cnt_dev = plan.lse.clone(), plan.decisions.clone(), plan.counters.clone()
+    plan.o.zero_()
+    plan.lse.zero_()
+    plan.decisions.zero_()
+    oh = torch.empty_like(q).pin_memory()
+    plan.run_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, o_dev.cpu())
+    assert torch.equal(plan.lse, lse_dev) and torch.equal(plan.decisions, dec_dev)
+    assert torch.equal(plan.counters[:2], cnt_dev[:2])
+    assert 0 < int(cnt_dev[1]) < int(cnt_dev[0])
+    with pytest.raises(bsfa.ConfigurationError):
+        plan.run_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, chunks=3)
