@@ -20,5 +20,6 @@ from .trace import FRONTIER, KEPT, SKIPPED, UNREACHABLE, GateTrace
 from .attention import AttentionResult, BsfaPlan, attention, flash_forward, reference_scale
 from .calibration import (BlockMaximaProfile, CalibrationDiagnostics, CalibrationDump,
                           CalibrationSample, Calibrator, calibrate, collect_block_maxima)
+from .dump import MANIFEST_NAME, load_dump, save_dump, write_model_dump
 
 __version__ = "0.1.0"

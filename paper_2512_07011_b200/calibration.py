@@ -33,6 +33,8 @@ from .tiling import TileConfig, off_frontier_count, require_kernel_tiles
 def _to_array(x):
     if isinstance(x, torch.Tensor):
         return x
+    if isinstance(x, np.ndarray) and x.dtype == np.float32:
+        return x  # views (e.g. memory-mapped dump blobs) stay lazy; uploads copy per layer
     return np.ascontiguousarray(x, dtype=np.float32)
 
 

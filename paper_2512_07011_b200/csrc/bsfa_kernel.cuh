@@ -48,6 +48,11 @@
 #ifndef BSFA_EXP_CHAIN
 #define BSFA_EXP_CHAIN 1
 #endif
+// Turn-taking between the two query tiles' softmax groups (NQ = 2): 0 = free
+// running, 1 = the exponential phases alternate, 2 = whole steps alternate.
+#ifndef BSFA_TURN
+#define BSFA_TURN 0
+#endif
 // Debug timeline (bsfa_debug_trace); compiled out of the production library.
 #ifndef BSFA_TRACE
 #define BSFA_TRACE 0
@@ -749,7 +754,17 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     unsigned dn = 0;
     unsigned long long kept_tiles = 0;
 
+    // turn barriers 5 + s: group s may start its phase once the other group
+    // finished the same phase of the previous (s = 0) / same (s = 1) step
+    constexpr bool kTurn = !CALIB && NQ == 2 && BSFA_TURN != 0;
+    auto turn_wait = [&](int j) {
+      if (kTurn && !(s == 0 && j == 0)) named_bar_sync(5 + s, 256);
+    };
+    auto turn_pass = [&]() {
+      if (kTurn) named_bar_arrive(5 + (s ^ 1), 256);
+    };
     for (int j = 0; j < nsteps; ++j) {
+      if (BSFA_TURN == 2) turn_wait(j);
       mbar_wait((s_full + 8 * (s)), j & 1);
       if (tr0 && j < kTraceSteps) p.trace[(kEvSReady * 2 + s) * kTraceSteps + j] = clock64();
       tc_fence_after();
@@ -871,8 +886,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
             mbar_arrive((p_half + 8 * (1)));
           }
           if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
+          if (BSFA_TURN == 1) turn_wait(j);
+          turn_pass();
           continue;
         }
+        if (BSFA_TURN == 1) turn_wait(j);
 
         float m_step = -INFINITY;
 #pragma unroll
@@ -954,6 +972,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           if (tr0 && hh == 0 && j < kTraceSteps) p.trace[(kEvExpDone * 2 + s) * kTraceSteps + j] = clock64();
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
+        turn_pass();
 
         // row sum of the kept exponentials (off the MMA critical path)
         uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
@@ -975,6 +994,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         o_valid = true;
       }
     }
+    if (kTurn && s == 0 && nsteps > 0) named_bar_sync(5, 256);  // group 1's last pass
 
     if constexpr (CALIB) {
       // ---- order statistics of this row of gate-tile maxima (calibration.py:116-153)

@@ -533,3 +533,21 @@ def test_plan_run_host_matches_device_run(bsfa, B, hq, hkv, chunks):
     assert 0 < int(cnt_dev[1]) < int(cnt_dev[0])
     with pytest.raises(bsfa.ConfigurationError):
         plan.run_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, chunks=3)
+
+
+def test_calibrate_from_dump_directory(bsfa, tmp_path):
+    """GPU-generated dump written in the reference format, mapped back and
+    calibrated layer by layer == calibrating the same arrays in memory == oracle."""
+    tiles = bsfa.TileConfig(128, 64)
+    bsfa.write_model_dump(tmp_path, 2, 2, 4, 1024, 64, seed=3, device="cuda")
+    dump = bsfa.load_dump(tmp_path)
+    t_disk = bsfa.calibrate(dump, [2, 5], tiles)
+    mem = bsfa.CalibrationDump(2, 4, 64, [bsfa.CalibrationSample(s.sample_id, np.array(s.q), np.array(s.k))
+                                          for s in dump.samples])
+    t_mem = bsfa.calibrate(mem, [2, 5], tiles)
+    np.testing.assert_array_equal(t_disk.values, t_mem.values)
+    samples = [(s.sample_id, orc.round_bf16(np.array(s.q)), orc.round_bf16(np.array(s.k))) for s in dump.samples]
+    ref, _, _ = orc.calibrate(samples, [2, 5], 128, 64)
+    fin = np.isfinite(ref)
+    np.testing.assert_array_equal(np.isfinite(t_disk.values), fin)
+    assert np.abs(t_disk.values[fin] - ref[fin]).max() <= 1e-4
