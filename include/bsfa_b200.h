@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BSFA_ABI_VERSION 3
+#define BSFA_ABI_VERSION 4
 
 /* error codes */
 #define BSFA_OK 0
@@ -54,6 +54,8 @@ extern "C" {
 #define BSFA_CNT_VLOADS 2    /* V gate tiles fetched by TMA (one fetch serves    */
                              /* every query tile of a CTA that kept the tile)  */
 #define BSFA_CNT_VUNITS 3    /* V gate tiles a CTA could have fetched           */
+
+#define BSFA_MAX_O_PEERS 7 /* a gather over up to 8 GPUs */
 
 typedef struct bsfa_fwd_args {
   /* inputs: bf16 [batch][heads][seq][head_dim], arbitrary element strides with
@@ -83,6 +85,11 @@ typedef struct bsfa_fwd_args {
   int inject_fault;
   int gate_window;   /* BSFA_GATE_WINDOW: trailing window w >= 0 (tokens) */
   float gate_lambda; /* BSFA_GATE_RUNMAX: keep iff max_rows(local - running max) >= lambda */
+  /* extra O destinations written by the epilogue with o's strides and the same
+     element offsets (e.g. other GPUs' gathered-O buffers mapped over NVLink), so
+     a head-sharded forward needs no separate all-gather; 0..BSFA_MAX_O_PEERS */
+  int num_o_peers;
+  void* o_peers[BSFA_MAX_O_PEERS];
 } bsfa_fwd_args;
 
 typedef struct bsfa_calib_args {

@@ -16,7 +16,8 @@ from .errors import BsfaError
 LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
+MAX_O_PEERS = 7
 
 BSFA_OK = 0
 BSFA_ERR_INVALID = -1
@@ -74,6 +75,8 @@ class FwdArgs(ctypes.Structure):
         ("inject_fault", ctypes.c_int),
         ("gate_window", ctypes.c_int),
         ("gate_lambda", ctypes.c_float),
+        ("num_o_peers", ctypes.c_int),
+        ("o_peers", ctypes.c_void_p * 7),
     ]
 
 

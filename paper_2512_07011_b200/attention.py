@@ -109,7 +109,8 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
               k_level: int | None = None, head_offset: int = 0,
               tiles: TileConfig = TileConfig(), return_trace: bool = False,
               inject_fault: bool = False, check_numerics: bool = False,
-              scale: float | None = None) -> AttentionResult:
+              scale: float | None = None, out: torch.Tensor | None = None,
+              o_peers=()) -> AttentionResult:
     """Block-sparse (or dense) causal/non-causal GQA attention forward.
 
     Gate selection: ``thresholds`` + ``k_level`` (+ ``layer``) runs the
@@ -117,6 +118,12 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     ``values[level, layer, head_offset + h, min(i, P-1)]``; otherwise ``gate``
     may be a DenseGate / FrontierOnlyGate / ThresholdGate object; with
     neither the run is dense.
+
+    ``out`` (bf16 [B, Hq, n_pad, d_pad], unit head_dim stride, 16-byte aligned
+    rows) receives O instead of a fresh tensor; ``o_peers`` are device
+    addresses of further copies with ``out``'s strides (peer GPUs' slots of a
+    gathered-O buffer mapped over NVLink) that the kernel epilogue writes
+    alongside ``out`` -- the head-sharded all-gather without a collective.
     """
     _check_inputs(q, k, v)
     require_kernel_tiles(tiles)
@@ -153,7 +160,20 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         qk = _as_kernel_operand(q, n_pad, d_pad)
         kk = _as_kernel_operand(k, n_pad, d_pad)
         vk = _as_kernel_operand(v, n_pad, d_pad)
-        o = torch.empty((bsz, hq, n_pad, d_pad), dtype=torch.bfloat16, device=dev)
+        o_peers = [int(x) for x in o_peers]
+        if out is not None:
+            if (tuple(out.shape) != (bsz, hq, n_pad, d_pad) or out.dtype != torch.bfloat16 or out.device != dev
+                    or out.stride(3) != 1 or (out.stride(2) * 2) % 16 or out.data_ptr() % 16):
+                raise InvalidInputError(
+                    f"out must be bf16 {(bsz, hq, n_pad, d_pad)} on {dev} with unit head_dim stride and "
+                    "16-byte aligned rows")
+            o = out
+        elif o_peers:
+            raise InvalidInputError("o_peers mirror out's layout: pass out as well")
+        else:
+            o = torch.empty((bsz, hq, n_pad, d_pad), dtype=torch.bfloat16, device=dev)
+        if len(o_peers) > _lib.MAX_O_PEERS:
+            raise ConfigurationError(f"at most {_lib.MAX_O_PEERS} peer copies of O")
         lse = torch.empty((bsz, hq, n_pad), dtype=torch.float32, device=dev)
         m_q, m_kv = n_pad // tiles.b_m, n_pad // tiles.b_n
         dec = torch.zeros((bsz, hq, m_q, m_kv), dtype=torch.int8, device=dev) if return_trace else None
@@ -181,6 +201,9 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         a.scale = sc
         a.inject_fault = 1 if inject_fault else 0
         a.gate_window, a.gate_lambda = gate_params(gate) if thr_dev is None else (0, 0.0)
+        a.num_o_peers = len(o_peers)
+        for i, ptr in enumerate(o_peers):
+            a.o_peers[i] = ptr
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(_lib.load_library().bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
 

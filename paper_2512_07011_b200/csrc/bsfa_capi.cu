@@ -14,6 +14,8 @@
 #endif
 #include "bsfa_kernel_gs.cuh"
 
+static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
+
 using namespace bsfa;
 
 namespace {
@@ -240,6 +242,14 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.o_sb = a->o_stride_b;
   p.o_sh = a->o_stride_h;
   p.o_sn = a->o_stride_n;
+  if (a->num_o_peers < 0 || a->num_o_peers > BSFA_MAX_O_PEERS)
+    return fail(BSFA_ERR_INVALID, "num_o_peers %d outside [0, %d]", a->num_o_peers, BSFA_MAX_O_PEERS);
+  p.num_o_peers = a->num_o_peers;
+  for (int i = 0; i < a->num_o_peers; ++i) {
+    if (!a->o_peers[i] || reinterpret_cast<uintptr_t>(a->o_peers[i]) % 16)
+      return fail(BSFA_ERR_INVALID, "o_peers[%d] must be a 16-byte aligned device pointer", i);
+    p.o_peer[i] = reinterpret_cast<__nv_bfloat16*>(a->o_peers[i]);
+  }
   p.lse = a->lse;
   p.trace = g_trace;
   p.trace_cta = g_trace_cta;

@@ -99,7 +99,22 @@ struct KernelParams {
   // debug: per-step clock64 timestamps of one CTA (bsfa_debug_trace)
   long long* trace;
   int trace_cta;
+  // extra O destinations (peer GPUs' gathered-O buffers), same element offsets
+  int num_o_peers;
+  __nv_bfloat16* o_peer[7];
 };
+
+// 16 packed bf16x2 words (32 O elements of one row) -> O and every peer copy
+__device__ __forceinline__ void store_o32(const KernelParams& p, long long off, const uint32_t* pk) {
+  const uint4 w0 = make_uint4(pk[0], pk[1], pk[2], pk[3]), w1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  const uint4 w2 = make_uint4(pk[8], pk[9], pk[10], pk[11]), w3 = make_uint4(pk[12], pk[13], pk[14], pk[15]);
+  uint4* dst = reinterpret_cast<uint4*>(p.o + off);
+  dst[0] = w0, dst[1] = w1, dst[2] = w2, dst[3] = w3;
+  for (int i = 0; i < p.num_o_peers; ++i) {
+    uint4* pd = reinterpret_cast<uint4*>(p.o_peer[i] + off);
+    pd[0] = w0, pd[1] = w1, pd[2] = w2, pd[3] = w3;
+  }
+}
 
 // trace slots: trace[(ev * 2 + s) * kTraceSteps + j]
 constexpr int kTraceSteps = 2048;
@@ -690,8 +705,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       const float inv_l = 1.f / l_row;
       bool bad = !(l_row > 0.f);
       const int row = qi * 128 + r;
-      __nv_bfloat16* orow =
-          p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + h * (D / 2);
+      const long long orow = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn + h * (D / 2);
 #pragma unroll
       for (int c = 0; c < D / 2; c += 32) {
         uint32_t ov[32];
@@ -705,9 +719,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           bad |= !isfinite(a0) || !isfinite(a1);
           pk[e / 2] = pack_bf16x2(a0, a1);
         }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        store_o32(p, orow + c, pk);
       }
       if (h == 0) p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_row);
       if (bad && p.status) atomicOr(p.status, 1);
@@ -1053,7 +1065,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       const float inv_l = 1.f / l_sum;
       bool bad = !(l_sum > 0.f);
       const int row = qi * 128 + r;
-      __nv_bfloat16* orow = p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
+      const long long orow = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t ov[32];
@@ -1067,9 +1079,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           bad |= !isfinite(a0) || !isfinite(a1);
           pk[e / 2] = pack_bf16x2(a0, a1);
         }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        store_o32(p, orow + c, pk);
       }
       p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
       if (bad && p.status) atomicOr(p.status, 1);

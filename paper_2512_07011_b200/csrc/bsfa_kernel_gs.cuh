@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(GsCfg<D, NQ, CALIB>::NUM_THREADS, 1)
       const float inv_l = 1.f / l_sum;
       bool bad = !(l_sum > 0.f);
       const int row = qi * 128 + r;
-      __nv_bfloat16* orow = p.o + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
+      const long long orow = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t ov[32];
@@ -584,9 +584,7 @@ __global__ void __launch_bounds__(GsCfg<D, NQ, CALIB>::NUM_THREADS, 1)
           bad |= !isfinite(a0) || !isfinite(a1);
           pk[e / 2] = pack_bf16x2(a0, a1);
         }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        store_o32(p, orow + c, pk);
       }
       p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
       if (bad && p.status) atomicOr(p.status, 1);

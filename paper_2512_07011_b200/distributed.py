@@ -5,9 +5,14 @@ reads only its own kv head, and thresholds are per (layer, head).  Rank r of
 W owns kv heads [r*Hkv/W, (r+1)*Hkv/W) and the q heads of those groups
 (a contiguous range, since q head h reads kv head h // (Hq/Hkv)), runs the
 ordinary kernel on them with ``head_offset`` selecting its threshold rows,
-and never talks to the other ranks during compute.  The only collective is
-an optional all-gather of O (NCCL over NVLink) when the caller needs the full
-[B, Hq, N, d] tensor on every rank.
+and never talks to the other ranks during compute.  When the caller needs the
+full [B, Hq, N, d] tensor on every rank there are two ways to assemble it:
+
+* ``gather="nccl"``: an all-gather of O after the kernel (NCCL over NVLink);
+* ``gather="peer"``: a :class:`PeerGatherBuffer` in symmetric memory -- the
+  kernel epilogue stores each rank's O rows into its own slot of every
+  rank's buffer over NVLink (``bsfa_fwd_args.o_peers``), so the exchange
+  overlaps the attention tile by tile and only a barrier follows.
 """
 
 from __future__ import annotations
@@ -65,17 +70,80 @@ def gather_heads(o_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
         dist.all_gather_into_tensor(buf.view(world * b, hl, n, d), src.view(b, hl, n, d), group=group)
     else:
         dist.all_gather(list(buf.unbind(0)), src, group=group)
+    return gathered_view(buf)  # head-major for B = 1: rank shards are already contiguous
+
+
+def peer_slot_pointers(buffer_ptrs, rank: int, slot_bytes: int) -> list[int]:
+    """Addresses of rank ``rank``'s slot in every OTHER rank's gathered-O buffer.
+
+    ``buffer_ptrs[p]`` is rank p's buffer base as mapped into this process
+    (symmetric memory); the buffer is rank-major [W, B, Hq/W, N, d].
+    """
+    return [int(base) + rank * slot_bytes for p, base in enumerate(buffer_ptrs) if p != rank]
+
+
+def gathered_view(buf: torch.Tensor) -> torch.Tensor:
+    """Rank-major [W, B, Hq/W, N, d] -> [B, Hq, N, d] (a view for B = 1)."""
+    world, b, hl, n, d = buf.shape
     if b == 1:
-        return buf.view(1, world * hl, n, d)  # head-major: rank shards are already contiguous
+        return buf.view(1, world * hl, n, d)
     return buf.permute(1, 0, 2, 3, 4).reshape(b, world * hl, n, d)
 
 
+class PeerGatherBuffer:
+    """Gathered O, rank-major [W, B, Hq/W, N, d], filled by the kernel epilogues of all ranks.
+
+    ``out`` is this rank's slot (pass it as ``attention(out=...)``) and
+    ``peers`` the addresses of this rank's slot in the other ranks' buffers
+    (``attention(o_peers=...)``).  After every rank's launch, :meth:`barrier`
+    orders the remote stores before anyone reads :meth:`gathered`.
+    Build it with :meth:`symmetric` (torch symmetric memory over NVLink);
+    the constructor takes any mapping of the W buffers (tests use shared CPU
+    memory and gloo).
+    """
+
+    def __init__(self, buf: torch.Tensor, buffer_ptrs, rank: int, barrier):
+        world = buf.shape[0]
+        if len(buffer_ptrs) != world or not 0 <= rank < world:
+            raise ConfigurationError(f"{len(buffer_ptrs)} buffers for rank {rank} of {world}")
+        if world - 1 > 7:
+            raise ConfigurationError("peer stores reach at most 7 other GPUs")
+        self.buf, self.rank, self.world = buf, rank, world
+        self.out = buf[rank]
+        self.peers = peer_slot_pointers(buffer_ptrs, rank, self.out.numel() * self.out.element_size())
+        self._barrier = barrier
+
+    @classmethod
+    def symmetric(cls, batch: int, heads_q: int, seq_len: int, head_dim: int, *, rank: int, world: int,
+                  group=None, device=None) -> "PeerGatherBuffer":
+        from torch.distributed import _symmetric_memory as symm_mem
+
+        if heads_q % world:
+            raise ConfigurationError(f"{heads_q} q heads cannot be split over {world} ranks")
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        buf = symm_mem.empty((world, batch, heads_q // world, seq_len, head_dim), dtype=torch.bfloat16,
+                             device=device)
+        grp = group if group is not None else dist.group.WORLD
+        handle = symm_mem.rendezvous(buf, grp.group_name)
+        self = cls(buf, [int(x) for x in handle.buffer_ptrs], rank, lambda: handle.barrier())
+        self.handle = handle
+        return self
+
+    def barrier(self) -> None:
+        self._barrier()
+
+    def gathered(self) -> torch.Tensor:
+        return gathered_view(self.buf)
+
+
 def sharded_attention(q, k, v, *, rank: int, world: int, thresholds=None, layer: int = 0,
-                      k_level=None, gather: bool = False, group=None, compute=None, **kw):
+                      k_level=None, gather=False, group=None, compute=None, peer_buffer=None, **kw):
     """Run this rank's heads of a full [B, Hq, N, d] problem.
 
     ``q``/``k``/``v`` may be the full tensors (sliced here) or already the
-    local shard (``q.shape[1] == Hq/W``).  ``compute`` defaults to
+    local shard (``q.shape[1] == Hq/W``).  ``gather``: False, True/"nccl"
+    (all-gather after the kernel) or "peer" (epilogue stores into
+    ``peer_buffer``, a :class:`PeerGatherBuffer`).  ``compute`` defaults to
     :func:`attention`; tests substitute a CPU checker to exercise the
     partition/gather logic without a GPU.
     """
@@ -91,6 +159,13 @@ def sharded_attention(q, k, v, *, rank: int, world: int, thresholds=None, layer:
         q = q[:, sh.q_lo:sh.q_hi]
         k = k[:, sh.kv_lo:sh.kv_hi]
         v = v[:, sh.kv_lo:sh.kv_hi]
+    if gather == "peer":
+        if peer_buffer is None:
+            raise ConfigurationError('gather="peer" needs a PeerGatherBuffer')
+        res = compute(q, k, v, thresholds=thresholds, layer=layer, k_level=k_level, head_offset=sh.q_lo,
+                      out=peer_buffer.out, o_peers=peer_buffer.peers, **kw)
+        peer_buffer.barrier()
+        return res, peer_buffer.gathered()
     res = compute(q, k, v, thresholds=thresholds, layer=layer, k_level=k_level, head_offset=sh.q_lo, **kw)
     if gather:
         return res, gather_heads(res.o, world, group)

@@ -98,3 +98,56 @@ def test_two_rank_gather_matches_single_process(batch):
 def test_gather_single_rank_is_identity():
     x = torch.randn(1, 2, 8, 4)
     assert gather_heads(x, 1) is x
+
+
+def _peer_compute(q, k, v, out=None, o_peers=(), **kw):
+    """The epilogue's contract on CPU: O into `out` and byte-identical copies at every peer address."""
+    import ctypes
+    res = _oracle_compute(q, k, v, **kw)
+    out.copy_(res.o)
+    for ptr in o_peers:
+        ctypes.memmove(ptr, out.data_ptr(), out.numel() * out.element_size())
+    return res
+
+
+def _peer_worker(rank, world, port, bufs, q, k, v, thr, expected, result_q):
+    from paper_2512_07011_b200.distributed import PeerGatherBuffer
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pb = PeerGatherBuffer(bufs[rank], [b.data_ptr() for b in bufs], rank, dist.barrier)
+        assert pb.peers == [bufs[p].data_ptr() + rank * pb.out.numel() * 4 for p in range(world) if p != rank]
+        _, full = sharded_attention(q, k, v, rank=rank, world=world, thresholds=thr, layer=1, k_level=4,
+                                    gather="peer", peer_buffer=pb, compute=_peer_compute)
+        result_q.put((rank, tuple(full.shape), float((full - expected).abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_two_rank_peer_gather(batch):
+    """gather="peer": each rank's rows land in its slot of BOTH ranks' buffers (rank-major layout)."""
+    import paper_2512_07011_b200 as bsfa
+    rng = np.random.default_rng(10 + batch)
+    hq, hkv, n, d = 4, 2, 256, 16
+    q = torch.from_numpy(rng.standard_normal((batch, hq, n, d)).astype(np.float32))
+    k = torch.from_numpy(rng.standard_normal((batch, hkv, n, d)).astype(np.float32))
+    v = torch.from_numpy(rng.standard_normal((batch, hkv, n, d)).astype(np.float32))
+    vals = rng.uniform(0.5, 1.0, size=(1, 2, hq, 2)).astype(np.float32)
+    thr = bsfa.ThresholdTensor(values=vals, k_levels=(4,), n_max=256, b_m=128, b_n=64)
+    expected = _oracle_compute(q, k, v, thresholds=thr, layer=1, k_level=4).o
+    bufs = [torch.zeros((2, batch, hq // 2, n, d)).share_memory_() for _ in range(2)]
+    ctx = mp.get_context("fork")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, bufs, q, k, v, thr, expected, result_q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    results = sorted(result_q.get(timeout=10) for _ in range(2))
+    for rank, shape, err in results:
+        assert shape == (batch, hq, n, d)
+        assert err == 0.0, (rank, err)

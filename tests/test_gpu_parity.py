@@ -551,3 +551,59 @@ def test_calibrate_from_dump_directory(bsfa, tmp_path):
     fin = np.isfinite(ref)
     np.testing.assert_array_equal(np.isfinite(t_disk.values), fin)
     assert np.abs(t_disk.values[fin] - ref[fin]).max() <= 1e-4
+
+
+def test_epilogue_peer_copies(bsfa):
+    """o_peers: the epilogue writes every O row to each extra destination too (the NVLink gather path)."""
+    rng = np.random.default_rng(21)
+    B, hq, hkv, n, d = 2, 4, 2, 1024, 128
+    q, k, v = (_dev(rng.standard_normal(s).astype(np.float32)) for s in ((B, hq, n, d), (B, hkv, n, d), (B, hkv, n, d)))
+    ref = bsfa.attention(q, k, v).o
+    out = torch.empty_like(ref)
+    peers = [torch.full_like(ref, float("nan")) for _ in range(3)]
+    res = bsfa.attention(q, k, v, out=out, o_peers=[p.data_ptr() for p in peers])
+    assert res.o.data_ptr() == out.data_ptr() and torch.equal(out, ref)
+    for p in peers:
+        assert torch.equal(p, ref)
+    with pytest.raises(bsfa.InvalidInputError):
+        bsfa.attention(q, k, v, o_peers=[peers[0].data_ptr()])
+
+
+_PEER_SCRIPT = r"""
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import paper_2512_07011_b200 as bsfa
+from paper_2512_07011_b200.distributed import PeerGatherBuffer, sharded_attention
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=sys.argv[1])
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+g = torch.Generator(device="cuda").manual_seed(5)
+q = torch.randn(1, 8, 2048, 128, device="cuda", generator=g).bfloat16()
+k = torch.randn(1, 2, 2048, 128, device="cuda", generator=g).bfloat16()
+v = torch.randn(1, 2, 2048, 128, device="cuda", generator=g).bfloat16()
+pb = PeerGatherBuffer.symmetric(1, 8, 2048, 128, rank=0, world=1)
+assert pb.peers == []
+_, full = sharded_attention(q, k, v, rank=0, world=1, gather="peer", peer_buffer=pb)
+assert torch.equal(full, bsfa.attention(q, k, v).o)
+dist.destroy_process_group()
+print("PEER_OK")
+"""
+
+
+def test_symmetric_peer_buffer_single_rank(tmp_path):
+    """The symmetric-memory plumbing of gather="peer" on a one-rank NCCL group (own process)."""
+    import socket
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    script = tmp_path / "peer.py"
+    script.write_text(_PEER_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, str(script), str(port)], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert "PEER_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
