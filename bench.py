@@ -63,8 +63,9 @@ def parse_args():
     ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
                     help="multi-GPU: batch = weak scaling (rank r owns batch element r); heads = strong scaling "
                          "over kv-head groups of one batch-1 problem (configs[3])")
-    ap.add_argument("--gather", action="store_true",
-                    help="with --shard heads: all-gather O over NCCL inside every timed step")
+    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "peer"],
+                    help="with --shard heads: assemble the full O on every rank inside every timed step -- "
+                         "nccl: all-gather after the kernel; peer: epilogue stores into symmetric memory")
     return ap.parse_args()
 
 
@@ -348,6 +349,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     head_offset = 0
     gather_buf = None
+    peer_buf = None
     if args.shard == "heads" and world > 1:
         # strong scaling: rank r owns kv heads [r*Hkv/W, (r+1)*Hkv/W) of one problem
         from paper_2512_07011_b200.distributed import shard_heads
@@ -358,18 +360,24 @@ def main():
         v = vf[:, sh.kv_lo:sh.kv_hi].contiguous()
         del qf, kf, vf
         hq, hkv, head_offset = sh.num_q, sh.num_kv, sh.q_lo
-        if args.gather:
+        if args.gather == "nccl":
             gather_buf = torch.empty((world * hq, n, d), dtype=torch.bfloat16, device=dev)
+        elif args.gather == "peer":
+            from paper_2512_07011_b200.distributed import PeerGatherBuffer
+            peer_buf = PeerGatherBuffer.symmetric(1, world * hq, n, d, rank=rank, world=world, device=dev)
     else:
         q, k, v = make_inputs(cfg, rank, dev)  # rank r = batch element r (weak scaling)
     plan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level, head_offset=head_offset,
-                         device=dev)
+                         device=dev, out=peer_buf.out if peer_buf is not None else None,
+                         o_peers=peer_buf.peers if peer_buf is not None else ())
 
     def step():
         o = plan.run(q, k, v)
         if gather_buf is not None:
             import torch.distributed as dist
             dist.all_gather_into_tensor(gather_buf, o.view(hq, n, d))
+        if peer_buf is not None:
+            peer_buf.barrier()
 
     barrier(world)
     torch.cuda.synchronize()
@@ -442,8 +450,10 @@ def main():
                        "global_batch": 1 if (args.shard == "heads" and world > 1) else world, **cfg,
                        "tiles": "128x64", "causal": True, "k_level": k_level,
                        "predicted_density": costs.predicted_density(n, tiles, k_level),
-                       "parallelism": (f"kv-head-group sharding x{world}" + (", NCCL all-gather of O per step"
-                                       if gather_buf is not None else ", no collective"))
+                       "parallelism": (f"kv-head-group sharding x{world}" + (
+                           ", NCCL all-gather of O per step" if gather_buf is not None else
+                           ", O stored into every rank's symmetric buffer by the epilogue (NVLink)"
+                           if peer_buf is not None else ", no collective"))
                        if (args.shard == "heads" and world > 1) else f"batch sharding x{world}, no collective",
                        "l2": "inputs (Q/K/V 384 MiB at 32K) exceed the 126 MB L2; no explicit flush",
                        "thresholds": "calibrated on a separate synthetic sample (seed 1000)"},

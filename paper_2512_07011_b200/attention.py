@@ -264,7 +264,8 @@ class BsfaPlan:
     def __init__(self, batch: int, heads_q: int, heads_kv: int, seq_len: int, head_dim: int, *,
                  causal: bool = True, tiles: TileConfig = TileConfig(), thresholds: ThresholdTensor | None = None,
                  layer: int = 0, k_level: int | None = None, head_offset: int = 0, gate=None,
-                 return_trace: bool = False, device=None):
+                 return_trace: bool = False, device=None, out: torch.Tensor | None = None, o_peers=()):
+        """``out`` / ``o_peers``: as in :func:`attention` (caller-owned O, extra peer copies)."""
         require_kernel_tiles(tiles)
         if head_dim not in (64, 128):
             raise InvalidInputError("plans take head_dim 64 or 128 (pad smaller heads)")
@@ -292,7 +293,18 @@ class BsfaPlan:
             mode = kernel_gate_mode(gate)
         else:
             mode = _lib.GATE_DENSE
-        self.o = torch.empty(self.shape_q, dtype=torch.bfloat16, device=dev)
+        o_peers = [int(x) for x in o_peers]
+        if out is not None:
+            if (tuple(out.shape) != self.shape_q or out.dtype != torch.bfloat16 or out.device != dev
+                    or out.stride(3) != 1 or (out.stride(2) * 2) % 16 or out.data_ptr() % 16):
+                raise InvalidInputError(f"out must be bf16 {self.shape_q} on {dev} with 16-byte aligned rows")
+            self.o = out
+        elif o_peers:
+            raise InvalidInputError("o_peers mirror out's layout: pass out as well")
+        else:
+            self.o = torch.empty(self.shape_q, dtype=torch.bfloat16, device=dev)
+        if len(o_peers) > _lib.MAX_O_PEERS:
+            raise ConfigurationError(f"at most {_lib.MAX_O_PEERS} peer copies of O")
         self.lse = torch.empty((batch, heads_q, self.n_pad), dtype=torch.float32, device=dev)
         m_q, m_kv = self.n_pad // tiles.b_m, self.n_pad // tiles.b_n
         self.decisions = (torch.zeros((batch, heads_q, m_q, m_kv), dtype=torch.int8, device=dev)
@@ -316,6 +328,9 @@ class BsfaPlan:
         a.scale = reference_scale(head_dim)
         a.inject_fault = 0
         a.gate_window, a.gate_lambda = gate_params(gate) if self.thr is None else (0, 0.0)
+        a.num_o_peers = len(o_peers)
+        for i, ptr in enumerate(o_peers):
+            a.o_peers[i] = ptr
         self.args = a
         self.lib = _lib.load_library()
 
