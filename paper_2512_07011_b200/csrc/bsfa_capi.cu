@@ -9,10 +9,15 @@
 
 #include "../../include/bsfa_b200.h"
 #include "bsfa_kernel.cuh"
+// forward at b_n = 64: the Q-in-TMEM 64-key-step kernel (bsfa_kernel_qt.cuh)
+#ifndef BSFA_QT_FWD
+#define BSFA_QT_FWD 0
+#endif
 #ifndef BSFA_GATE_STEP
 #define BSFA_GATE_STEP 0
 #endif
 #include "bsfa_kernel_gs.cuh"
+#include "bsfa_kernel_qt.cuh"
 
 static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
 
@@ -121,6 +126,24 @@ int launch_gs(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& t
   return BSFA_OK;
 }
 
+template <int D, int NQ>
+int launch_qt(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+              cudaStream_t st) {
+  using C = QtCfg<D, NQ>;
+  auto kern = bsfa_kernel_qt<D, NQ>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  if (grid == 0) return BSFA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
+  return BSFA_OK;
+}
+
 // The 128-key-step kernel serves both gate widths (b_n = 64: two gate tiles
 // per step).  -DBSFA_GATE_STEP=1 builds the 64-key-step variant with a
 // double-buffered S ring instead (bsfa_kernel_gs.cuh; correct, tensor-bound,
@@ -134,6 +157,15 @@ int dispatch(int d, int b_n, int nq, const CUtensorMap& tq, const CUtensorMap& t
   if (d == D_ && b_n == 64 && nq == NQ_) return launch_gs<D_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
 #define BSFA_CASE(D_, BN_, NQ_) \
   if (d == D_ && b_n == BN_ && nq == NQ_) return launch<D_, 128 / BN_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
+#define BSFA_QT(D_, NQ_) \
+  if (d == D_ && b_n == 64 && nq == NQ_) return launch_qt<D_, NQ_>(tq, tk, tv, p, grid, st);
+  if constexpr (!CALIB && BSFA_QT_FWD) {
+    BSFA_QT(64, 1)
+    BSFA_QT(64, 2)
+    BSFA_QT(128, 1)
+    BSFA_QT(128, 2)
+  }
+#undef BSFA_QT
 #if BSFA_GATE_STEP
   BSFA_GS(64, 1)
   BSFA_GS(64, 2)
@@ -179,6 +211,16 @@ int bsfa_device_supported(void) {
   return prop.major == 10 && prop.minor == 0 ? 1 : 0;
 }
 
+#if BSFA_WATCHDOG_RECORD
+// debug builds only: stuck waits recorded by the watchdog (count, then records)
+extern "C" int bsfa_debug_stuck(unsigned long long* host_out, int n) {
+  unsigned cnt = 0;
+  cudaMemcpyFromSymbol(&cnt, bsfa_stuck_n, sizeof(cnt));
+  cudaMemcpyFromSymbol(host_out, bsfa_stuck, sizeof(unsigned long long) * (n < 64 ? n : 64));
+  return (int)cnt;
+}
+#endif
+
 int bsfa_debug_trace(long long* dev_buf, int cta) {
   g_trace = dev_buf;
   g_trace_cta = cta;
@@ -211,7 +253,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
-                       (BSFA_GATE_STEP && a->b_n == 64) ? 64 : 128, "k"))
+                       ((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64) ? 64 : 128, "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))

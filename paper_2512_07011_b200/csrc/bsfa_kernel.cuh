@@ -53,6 +53,12 @@
 #ifndef BSFA_TURN
 #define BSFA_TURN 0
 #endif
+// P of the second 64-key half in shared memory (PV from SMEM) instead of TMEM:
+// the next QK of a tile is issued right after the PV of the first half, so it
+// overlaps the second half's exponentials (S/P no longer alias across a step).
+#ifndef BSFA_P_SMEM
+#define BSFA_P_SMEM 1
+#endif
 // Debug timeline (bsfa_debug_trace); compiled out of the production library.
 #ifndef BSFA_TRACE
 #define BSFA_TRACE 0
@@ -133,7 +139,10 @@ struct KCfg {
 #ifndef BSFA_V_BYTES
 #define BSFA_V_BYTES 65536
 #endif
-  static constexpr int KS = D == 128 ? BSFA_K_STAGES : 3;
+  // second-half P in shared memory (forward, one thread per row)
+  static constexpr bool PSM = !CALIB && TPR == 1 && BSFA_P_SMEM != 0;
+  static constexpr int P_TILE = PSM ? 128 * 128 : 0;  // 128 rows x 64 keys bf16 per query tile
+  static constexpr int KS = D == 128 ? (PSM ? 2 : BSFA_K_STAGES) : 3;
   static constexpr int VS = CALIB ? 0 : (D == 128 ? BSFA_V_BYTES : 65536) / V_UNIT;
 #ifndef BSFA_DQ
 #define BSFA_DQ 4
@@ -143,10 +152,11 @@ struct KCfg {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQ * Q_TILE;
   static constexpr int OFF_V = OFF_K + KS * K_TILE;
-  static constexpr int OFF_CAL = OFF_V + VS * V_UNIT;
+  static constexpr int OFF_P = OFF_V + VS * V_UNIT;
+  static constexpr int OFF_CAL = OFF_P + NQ * P_TILE;
   static constexpr int CAL_BYTES = CALIB ? NQ * MAXA * 4 : 0;
   static constexpr int OFF_BAR = OFF_CAL + CAL_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 4 * NQ + 2 * NQ * DQ;
+  static constexpr int NUM_BARS = 1 + 2 * KS + 2 * VS + 4 * NQ + 2 * NQ * DQ + NQ;
   // per query tile: per-warp gate votes u32 [2 parity][4 warps]
   // per query tile (TPR = 2): half-row maxima f32 [2 parity][2 halves][128],
   // then the epilogue row sums f32 [2 halves][128]
@@ -226,6 +236,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
   const uint32_t sQ = sbase + C::OFF_Q;
   const uint32_t sK = sbase + C::OFF_K;
   const uint32_t sV = sbase + C::OFF_V;
+  const uint32_t sP = sbase + C::OFF_P;
   int* cvals = reinterpret_cast<int*>(smem + C::OFF_CAL);
   // mbarriers (8 bytes each)
   const uint32_t bar_q = sbase + C::OFF_BAR;
@@ -238,6 +249,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
   const uint32_t o_full = p_full + 16 * NQ;       // [NQ] last PV_s landed
   const uint32_t dec_full = o_full + 8 * NQ;      // [NQ][DQ]
   const uint32_t dec_empty = dec_full + 8 * NQ * DQ;
+  const uint32_t pv_done = dec_empty + 8 * NQ * DQ;  // [NQ] PSM: second-half PV_s(j) landed (P buffer free)
   const uint32_t xch_sm = sbase + C::OFF_XCH;
   const uint32_t dec_sm = sbase + C::OFF_DEC;
   const uint32_t decm_sm = sbase + C::OFF_DECM;
@@ -288,6 +300,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       mbar_init((dec_full + 8 * (i)), 1);
       mbar_init((dec_empty + 8 * (i)), 1);
     }
+    for (int s = 0; s < NQ; ++s) mbar_init((pv_done + 8 * (s)), 1);
     fence_mbarrier_init();
   }
   if constexpr (CALIB) {
@@ -393,6 +406,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       const uint64_t dq0 = make_sdesc_sw128(sQ, 16, 1024);
       const uint64_t dk0 = make_sdesc_sw128(sK, 16, 1024);
       const uint64_t dv0 = make_sdesc_sw128(sV, BN * 128, 1024);
+      const uint64_t dp0 = make_sdesc_sw128(sP, 16, 1024);
       mbar_wait(bar_q, 0);
 
       auto issue_qk = [&](int s, int j) {
@@ -410,6 +424,56 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 
       unsigned vbase = 0;      // V units consumed before this step
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
+      if constexpr (C::PSM) {
+        // Per step and tile: the first half (PV from TMEM, then the tile's next
+        // QK into S_s, which overlaps the second half's exponentials), then the
+        // second half (PV from shared memory).  V units are numbered at each
+        // tile's first half, in the producer's order (tile 0's keeps, then tile
+        // 1's additional ones).  (Serving both tiles' first halves before either
+        // second half was measured slower.)
+        uint32_t p1_par = 0;  // bit s: phase parity of p_full[s][1]
+        for (int j = 0; j < nsteps; ++j) {
+          const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
+          uint32_t prev = 0;
+          unsigned nunits = 0;
+          unsigned uidx[GT];
+#pragma unroll
+          for (int s = 0; s < NQ; ++s) {
+            mbar_wait((p_full + 8 * (2 * s)), j & 1);
+            tc_fence_after();
+            const uint32_t bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + s * 4);
+#pragma unroll
+            for (int x = 0; x < GT; ++x)
+              if (((bits & ~prev) >> x) & 1u) uidx[x] = vbase + nunits++;
+            prev |= bits;
+            if (bits & 1u) {
+              const unsigned u = uidx[0];
+              mbar_wait((v_full + 8 * (u % VS)), (u / VS) & 1);
+              umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::S_COL + s * 128,
+                          dv0 + uint64_t(((u % VS) * C::V_UNIT) >> 4), IDESC_PV, (o_started >> s) & 1u);
+              o_started |= 1u << s;
+            }
+            if (j + 1 < nsteps) issue_qk(s, j + 1);  // S_s is free once P half 0 is consumed
+            constexpr int x1 = GT == 2 ? 1 : 0;
+            if ((bits >> x1) & 1u) {
+              // released for kept second halves only: phase = this tile's count of them
+              mbar_wait((p_full + 8 * (2 * s + 1)), (p1_par >> s) & 1u);
+              p1_par ^= 1u << s;
+              tc_fence_after();
+              const unsigned u = uidx[x1];
+              if (GT == 2) mbar_wait((v_full + 8 * (u % VS)), (u / VS) & 1);
+              umma_pv64_ss_w(tmem + C::O_COL + s * D, dp0 + uint64_t((s * C::P_TILE) >> 4),
+                             dv0 + uint64_t(((u % VS) * C::V_UNIT) >> 4) + uint64_t(GT == 1 ? 512 : 0), IDESC_PV,
+                             (o_started >> s) & 1u);
+              o_started |= 1u << s;
+            }
+            umma_commit_w((pv_done + 8 * (s)));
+            if (j == nsteps - 1) umma_commit_w((o_full + 8 * (s)));
+          }
+          for (unsigned x = 0; x < nunits; ++x) umma_commit_w((v_empty + 8 * ((vbase + x) % VS)));
+          vbase += nunits;
+        }
+      } else {
       for (int j = 0; j < nsteps; ++j) {
         const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
         uint32_t prev = 0;     // gate tiles already assigned a V slot this step
@@ -460,6 +524,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           if (BSFA_TRACE && tr_cta && lane == 0 && j < kTraceSteps)
             p.trace[(kEvIssued * 2 + s) * kTraceSteps + j] = clock64();
         }
+      }
       }
     }
     __syncwarp();
@@ -893,10 +958,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         if (bits == 0) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive((p_half + 8 * (0)));
-            mbar_arrive((p_half + 8 * (1)));
-          }
+          if (lane == 0) mbar_arrive((p_half + 8 * (0)));
+          if (lane == 0 && !C::PSM) mbar_arrive((p_half + 8 * (1)));  // PSM: kept second halves only
           if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();
           if (BSFA_TURN == 1) turn_wait(j);
           turn_pass();
@@ -918,9 +981,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           m_ref = m_new;
           rescale = true;
         }
-        // O_s is quiescent here (S_s(j) committed after PV_s(j-1)): rescale the
-        // rows whose reference max moved by more than 2^8, before any P release
+        // O_s is quiescent here (S_s(j) committed after PV_s(j-1); PSM: after the
+        // first-half PV, pv_done certifies the second): rescale the rows whose
+        // reference max moved by more than 2^8, before any P release
         if (__any_sync(0xffffffffu, rescale)) {
+          if (C::PSM && j > 0) mbar_wait((pv_done + 8 * (s)), (j - 1) & 1);
           const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < D; c += 32) {
@@ -945,6 +1010,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const bool kept_h = ((bits >> (GT == 2 ? hh : 0)) & 1u) != 0;
+          // PSM: p_full[s][1] is released for kept second halves only (the MMA
+          // warp knows the decision); the previous step's second-half PV must
+          // have landed first -- it frees the P buffer and keeps p_full[s][1]
+          // at most one phase ahead of the MMA warp
+          if (C::PSM && hh == 1 && kept_h && j > 0) mbar_wait((pv_done + 8 * (s)), (j - 1) & 1);
           if (kept_h) {
             uint32_t pk[32];
 #pragma unroll
@@ -975,12 +1045,23 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
               pk[c / 2] = pack_bf16x2(p0, p1);
               pk[c / 2 + 1] = pack_bf16x2(p2, p3);
             }
-            tmem_st32(s_row + hh * 32, pk);
-            tmem_wait_st();
+            if (C::PSM && hh == 1) {
+              // second half -> shared memory, K-major SW128 (16-byte chunk c of
+              // row r at chunk c ^ (r & 7)); the buffer is free (pv_done waited below)
+              const uint32_t prow = sP + s * C::P_TILE + r * 128;
+#pragma unroll
+              for (int c16 = 0; c16 < 8; ++c16)
+                sts_u128(prow + ((c16 ^ (r & 7)) << 4), pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2],
+                         pk[4 * c16 + 3]);
+              fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+            } else {
+              tmem_st32(s_row + hh * 32, pk);
+              tmem_wait_st();
+            }
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive((p_half + 8 * (hh)));
+          if (lane == 0 && !(C::PSM && hh == 1 && !kept_h)) mbar_arrive((p_half + 8 * (hh)));
           if (tr0 && hh == 0 && j < kTraceSteps) p.trace[(kEvExpDone * 2 + s) * kTraceSteps + j] = clock64();
         }
         if (tr0 && j < kTraceSteps) p.trace[(kEvPDone * 2 + s) * kTraceSteps + j] = clock64();

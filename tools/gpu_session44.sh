@@ -1,0 +1,12 @@
+# Q-in-TMEM 64-key-step forward (BSFA_QT_FWD=1, + P_SMEM for b_n=128): parity + bench
+V=$PWD/paper_2512_07011_b200/_lib/variants
+export BSFA_LIB_PATH=$V/libbsfa_b200_qt.so
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "toy or dense_vs or golden_engine" 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | tail -4
+for i in 1 2; do
+  for t in psm qt; do
+    export BSFA_LIB_PATH=$V/libbsfa_b200_$t.so
+    timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/b44_$t.json 2>gpurun_out/b44_$t.err
+    python -c "import json; d=json.load(open('gpurun_out/b44_$t.json')); print('$t', round(d['ms_per_step'],3), round(d['value'],1), round(d['dense_ms_per_step'],3), round(d['dense_tflops'],1), round(d['speedup_vs_dense'],3))" || tail -3 gpurun_out/b44_$t.err
+  done
+done
