@@ -40,9 +40,11 @@
 #include "ptx.cuh"
 
 // Fraction of exponentials computed by polynomial on the FMA pipe instead of
-// the MUFU: 0 = none, 1 = 1/4, 2 = 1/2.
+// the MUFU: 0 = none, 1 = 1/4, 2 = 1/2.  With P's second half in shared memory
+// the softmax is issue-bound, not MUFU-bound: 0 measured fastest (l32k 6.23 ms
+// vs 6.34 at 1/4 and 7.16 at 1/2).
 #ifndef BSFA_EXP_EMU
-#define BSFA_EXP_EMU 1
+#define BSFA_EXP_EMU 0
 #endif
 // Order the polynomial exponentials after the same group's MUFU exponentials.
 #ifndef BSFA_EXP_CHAIN
