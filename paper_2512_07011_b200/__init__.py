@@ -21,5 +21,6 @@ from .attention import AttentionResult, BsfaPlan, attention, flash_forward, refe
 from .calibration import (BlockMaximaProfile, CalibrationDiagnostics, CalibrationDump,
                           CalibrationSample, Calibrator, calibrate, collect_block_maxima)
 from .dump import MANIFEST_NAME, load_dump, save_dump, write_model_dump
+from . import ops  # noqa: F401  (registers torch.ops.bsfa.*)
 
 __version__ = "0.1.0"

@@ -127,11 +127,9 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     """
     _check_inputs(q, k, v)
     require_kernel_tiles(tiles)
-    bsz, hq, n, d = q.shape
-    hkv = k.shape[1]
+    hq = q.shape[1]
 
     thr_dev = None
-    thr_positions = 0
     if thresholds is None and isinstance(gate, ThresholdGate):
         thresholds = gate.tensor
     if thresholds is not None:
@@ -142,7 +140,6 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
                 f"heads [{head_offset}, {head_offset + hq}) outside calibrated {thresholds.num_heads}")
         sl = thresholds.layer_slice(k_level, layer)[head_offset:head_offset + hq]
         thr_dev = torch.from_numpy(np.ascontiguousarray(sl)).to(q.device, non_blocking=False)
-        thr_positions = sl.shape[1]
         mode = _lib.GATE_THRESHOLD
     elif gate is not None:
         mode = kernel_gate_mode(gate)
@@ -150,7 +147,21 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
             raise ConfigurationError("threshold gate without thresholds")
     else:
         mode = _lib.GATE_DENSE
+    window, lam = gate_params(gate) if thr_dev is None else (0, 0.0)
+    res = _forward(q, k, v, thr_dev, mode, window, lam, causal=causal, tiles=tiles, return_trace=return_trace,
+                   inject_fault=inject_fault, scale=scale, out=out, o_peers=o_peers)
+    if check_numerics and int(res.status.item()) != 0:
+        raise NumericError("non-finite accumulator or zero normaliser in at least one query row")
+    return res
 
+
+def _forward(q, k, v, thr_dev, mode: int, window: int, lam: float, *, causal: bool, tiles: TileConfig,
+             return_trace: bool, inject_fault: bool = False, scale: float | None = None,
+             out: torch.Tensor | None = None, o_peers=()) -> AttentionResult:
+    """One ``bsfa_fwd`` launch on validated inputs; ``thr_dev`` fp32 [Hq, P] on q's device or None."""
+    bsz, hq, n, d = q.shape
+    hkv = k.shape[1]
+    thr_positions = int(thr_dev.shape[1]) if thr_dev is not None else 0
     n_pad = tiles.padded_len(n)
     d_pad = 64 if d <= 64 else 128
     sc = reference_scale(d) if scale is None else float(np.float32(scale))
@@ -200,7 +211,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         a.causal = 1 if causal else 0
         a.scale = sc
         a.inject_fault = 1 if inject_fault else 0
-        a.gate_window, a.gate_lambda = gate_params(gate) if thr_dev is None else (0, 0.0)
+        a.gate_window, a.gate_lambda = window, lam
         a.num_o_peers = len(o_peers)
         for i, ptr in enumerate(o_peers):
             a.o_peers[i] = ptr
@@ -210,8 +221,6 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     if n_pad != n or d_pad != d:
         o = o[:, :, :n, :d]
         lse = lse[:, :, :n]
-    if check_numerics and int(status.item()) != 0:
-        raise NumericError("non-finite accumulator or zero normaliser in at least one query row")
     return AttentionResult(o=o, lse=lse, decisions=dec, counters=counters, status=status)
 
 

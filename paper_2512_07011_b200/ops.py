@@ -1,0 +1,123 @@
+"""``torch.ops.bsfa`` custom operators over the C ABI (SURVEY §8(b) op contract).
+
+* ``bsfa::fwd(q, k, v, thr, causal, b_m, b_n, scale, want_trace)
+  -> (o, lse, counters, decisions)``: one ``bsfa_fwd`` launch.  ``thr`` is the
+  fp32 [Hq, P] slice ``values[level, layer]`` of a ThresholdTensor (one
+  threshold per (q head, query block), clamped at P - 1 as thresholds.py:87),
+  or an empty tensor for the DenseGate.  ``counters`` is int64 [4] (reachable,
+  kept, V tiles loaded, V tiles loadable); ``decisions`` the int8 code grid
+  [B, Hq, M_q, M_kv] (engine.py:22-25) when ``want_trace``, else empty.
+* ``bsfa::blockmax(q, k, b_m, b_n) -> bm``: fp32 [B, Hq, M_q, M_kv] of scaled
+  tile maxima over the off-frontier causal prefix j < A_i
+  (calibration.py:93-123), -inf elsewhere -- the calibration kernel (K2).
+* ``bsfa::calib_select(bm, k_levels) -> (thr, ties)``: per (head, position)
+  the (k+1)-th largest tile maximum with the reference's sentinels
+  (calibration.py:126-153): thr fp32 [S, B, Hq, M_q], ties int64 [S].
+
+The ops carry fake (meta) implementations, so they trace under
+``torch.compile`` / ``torch.export`` without running the kernel.  Only CUDA
+kernels are registered: the dispatcher refuses CPU tensors (no fallback).
+``calib_select`` is a selection utility over ``blockmax`` output built from
+torch ops; the calibration path itself (``calibrate`` / ``Calibrator``) fuses
+maxima, selection and accumulation in one kernel.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .attention import _check_inputs, _forward
+from .calibration import Calibrator
+from .errors import ConfigurationError, InvalidInputError
+from .tiling import TileConfig, require_kernel_tiles
+
+Tensor = torch.Tensor
+
+
+@torch.library.custom_op("bsfa::fwd", mutates_args=(), device_types="cuda")
+def fwd(q: Tensor, k: Tensor, v: Tensor, thr: Tensor, causal: bool, b_m: int, b_n: int, scale: float,
+        want_trace: bool) -> tuple[Tensor, Tensor, Tensor, Tensor]:
+    _check_inputs(q, k, v)
+    tiles = TileConfig(b_m, b_n)
+    require_kernel_tiles(tiles)
+    if thr.numel() == 0:
+        thr_dev, mode = None, _lib.GATE_DENSE
+    else:
+        if thr.dim() != 2 or thr.shape[0] != q.shape[1] or thr.dtype != torch.float32 or thr.device != q.device:
+            raise InvalidInputError(f"thr must be fp32 [Hq={q.shape[1]}, P] on {q.device}, got "
+                                    f"{thr.dtype} {tuple(thr.shape)} on {thr.device}")
+        thr_dev, mode = thr.contiguous(), _lib.GATE_THRESHOLD
+    res = _forward(q, k, v, thr_dev, mode, 0, 0.0, causal=causal, tiles=tiles, return_trace=want_trace,
+                   scale=scale)
+    o = res.o if res.o.is_contiguous() else res.o.contiguous()
+    lse = res.lse if res.lse.is_contiguous() else res.lse.contiguous()
+    dec = res.decisions if want_trace else q.new_empty((0,), dtype=torch.int8)
+    return o, lse, res.counters, dec
+
+
+@fwd.register_fake
+def _fwd_fake(q, k, v, thr, causal, b_m, b_n, scale, want_trace):
+    b, h, n, d = q.shape
+    n_pad = TileConfig(b_m, b_n).padded_len(n)
+    o = q.new_empty((b, h, n, d), dtype=torch.bfloat16)
+    lse = q.new_empty((b, h, n), dtype=torch.float32)
+    counters = q.new_empty((4,), dtype=torch.int64)
+    dec = (q.new_empty((b, h, n_pad // b_m, n_pad // b_n), dtype=torch.int8) if want_trace
+           else q.new_empty((0,), dtype=torch.int8))
+    return o, lse, counters, dec
+
+
+@torch.library.custom_op("bsfa::blockmax", mutates_args=(), device_types="cuda")
+def blockmax(q: Tensor, k: Tensor, b_m: int, b_n: int) -> Tensor:
+    _check_inputs(q, k, k)
+    tiles = TileConfig(b_m, b_n)
+    require_kernel_tiles(tiles)
+    b, h, n, d = q.shape
+    n_pad = tiles.padded_len(n)
+    out = torch.full((b, h, n_pad // b_m, n_pad // b_n), float("-inf"), dtype=torch.float32, device=q.device)
+    for bi in range(b):
+        cal = Calibrator([0], tiles, 1, h, n, d, device=q.device)
+        cal.add_layer(0, 0, q[bi], k[bi], seq_len=n, block_maxima=out[bi])
+    return out
+
+
+@blockmax.register_fake
+def _blockmax_fake(q, k, b_m, b_n):
+    b, h, n, _ = q.shape
+    n_pad = TileConfig(b_m, b_n).padded_len(n)
+    return q.new_empty((b, h, n_pad // b_m, n_pad // b_n), dtype=torch.float32)
+
+
+@torch.library.custom_op("bsfa::calib_select", mutates_args=(), device_types="cuda")
+def calib_select(bm: Tensor, k_levels: list[int], b_m: int, b_n: int) -> tuple[Tensor, Tensor]:
+    if bm.dim() != 4 or bm.dtype != torch.float32:
+        raise InvalidInputError(f"bm must be fp32 [B, H, M_q, M_kv], got {bm.dtype} {tuple(bm.shape)}")
+    if not k_levels or any(x < 0 for x in k_levels) or any(a >= c for a, c in zip(k_levels, k_levels[1:])):
+        raise ConfigurationError(f"k levels must be non-negative and strictly increasing: {list(k_levels)}")
+    m_q, m_kv = bm.shape[2], bm.shape[3]
+    # off-frontier prefix length A_p = p * b_m // b_n (tiling.py:63-65); entries past it are ignored
+    p = torch.arange(m_q, device=bm.device)
+    a_p = (p * b_m) // b_n
+    valid = torch.arange(m_kv, device=bm.device)[None, :] < a_p[:, None]
+    vals = torch.where(valid, bm, torch.full_like(bm, float("-inf")))
+    srt = torch.sort(vals, dim=-1, descending=True).values
+    thr, ties = [], []
+    for kk in k_levels:
+        if kk == 0:
+            thr.append(torch.full(bm.shape[:3], float("inf"), dtype=torch.float32, device=bm.device))
+            ties.append(torch.zeros((), dtype=torch.int64, device=bm.device))
+            continue
+        idx = min(kk, m_kv - 1)
+        cut = srt[..., idx] if kk < m_kv else torch.full(bm.shape[:3], float("-inf"), device=bm.device)
+        enough = (a_p > kk)[None, None, :]  # len(vals) > k (calibration.py:131-136)
+        thr.append(torch.where(enough, cut, torch.full_like(cut, float("-inf"))))
+        tie = enough & (srt[..., kk - 1] == srt[..., idx]) if kk < m_kv else torch.zeros_like(enough)
+        ties.append(tie.sum().to(torch.int64))
+    return torch.stack(thr), torch.stack(ties)
+
+
+@calib_select.register_fake
+def _calib_select_fake(bm, k_levels, b_m, b_n):
+    return (bm.new_empty((len(k_levels),) + tuple(bm.shape[:3]), dtype=torch.float32),
+            bm.new_empty((len(k_levels),), dtype=torch.int64))

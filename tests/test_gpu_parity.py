@@ -607,3 +607,45 @@ def test_symmetric_peer_buffer_single_rank(tmp_path):
     r = subprocess.run([sys.executable, str(script), str(port)], cwd=root, capture_output=True, text=True,
                        timeout=300)
     assert "PEER_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_torch_ops_match_python_api(bsfa):
+    """torch.ops.bsfa.fwd == attention() bit for bit; blockmax / calib_select == oracle."""
+    rng = np.random.default_rng(33)
+    B, hq, hkv, n, d = 2, 4, 2, 1000, 64  # ragged length: padded inside the op
+    qn = orc.round_bf16(rng.standard_normal((B, hq, n, d)).astype(np.float32))
+    kn = orc.round_bf16(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    vn = orc.round_bf16(rng.standard_normal((B, hkv, n, d)).astype(np.float32))
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    P = 8
+    vals = (3.3 + 0.2 * rng.standard_normal((1, 1, hq, P))).astype(np.float32)
+    t = bsfa.ThresholdTensor(values=vals, k_levels=(4,), n_max=1024, b_m=128, b_n=64)
+    ref = bsfa.attention(q, k, v, thresholds=t, k_level=4, return_trace=True)
+    thr = torch.from_numpy(vals[0, 0]).cuda()
+    o, lse, cnt, dec = torch.ops.bsfa.fwd(q, k, v, thr, True, 128, 64, bsfa.reference_scale(d), True)
+    assert torch.equal(o, ref.o) and torch.equal(lse, ref.lse) and torch.equal(dec, ref.decisions)
+    assert torch.equal(cnt, ref.counters)
+    od, _, _, nodec = torch.ops.bsfa.fwd(q, k, v, thr[:0], True, 128, 64, bsfa.reference_scale(d), False)
+    assert nodec.numel() == 0 and torch.equal(od, bsfa.attention(q, k, v).o)
+    # block maxima of the off-frontier prefix, then the (k+1)-th largest per position
+    g = hq // hkv
+    bm = torch.ops.bsfa.blockmax(q, k, 128, 64)
+    levels = [0, 2, 5]
+    thr_sel, ties = torch.ops.bsfa.calib_select(bm, levels, 128, 64)
+    bm_h, thr_h = bm.cpu().numpy(), thr_sel.cpu().numpy()
+    n_ties = [0] * len(levels)
+    for b in range(B):
+        for h in range(hq):
+            prof = orc.block_maxima(qn[b, h], kn[b, h // g], 128, 64)
+            for p, desc in enumerate(prof):
+                got = np.sort(bm_h[b, h, p, :len(desc)])[::-1]
+                np.testing.assert_allclose(got, desc, atol=1e-3, rtol=1e-5)
+                assert np.all(np.isneginf(bm_h[b, h, p, len(desc):]))
+                for li, kk in enumerate(levels):
+                    want = orc.cutoff(desc, kk)
+                    if np.isfinite(want):
+                        assert abs(thr_h[li, b, h, p] - want) <= 1e-3
+                    else:
+                        assert thr_h[li, b, h, p] == want
+                    n_ties[li] += orc.is_tie(np.sort(bm_h[b, h, p, :len(desc)])[::-1], kk)
+    assert ties.cpu().tolist() == n_ties
