@@ -364,12 +364,15 @@ class BsfaPlan:
                  chunks: int | None = None) -> torch.Tensor:
         """End-to-end forward from pinned host tensors into a pinned host output.
 
-        The problem is cut into ``chunks`` groups of kv heads (each with its
-        q heads); three CUDA streams pipeline host->device copies of group
-        c+1, the kernel on group c and the device->host copy of group c-1, so
-        PCIe transfers overlap the attention instead of bracketing it.  Inputs
-        are bf16 [B, H, n_pad, d] pinned host tensors of the plan's shape.
-        Returns ``o_h``; the caller synchronises (or waits on ``self.done``).
+        The q heads are cut into ``chunks`` equal groups (each within one kv
+        head or covering whole kv heads); streams pipeline the host->device
+        copy of group c+1, the kernel on group c (two compute streams, so one
+        launch's tail overlaps the next launch) and the device->host copy of
+        group c-1, so PCIe transfers overlap the attention instead of
+        bracketing it.  K/V of a kv head are copied with its first group.
+        Inputs are bf16 [B, H, n_pad, d] pinned host tensors of the plan's
+        shape.  Returns ``o_h``; the caller synchronises (or waits on
+        ``self.done``).
         """
         if tuple(q_h.shape) != self.shape_q or tuple(k_h.shape) != self.shape_kv or tuple(v_h.shape) != self.shape_kv:
             raise InvalidInputError(f"plan built for q{self.shape_q} kv{self.shape_kv}")
@@ -380,34 +383,48 @@ class BsfaPlan:
                 raise InvalidInputError("run_host takes contiguous bf16 host tensors (pinned for async copies)")
         bsz, hq, n, d = self.shape_q
         hkv = self.shape_kv[1]
+        grp = hq // hkv
+
+        def valid(c):
+            qp = hq // c
+            return hq % c == 0 and (qp % grp == 0 or grp % qp == 0)
+
         if chunks is None:
-            chunks = max(c for c in range(1, 9) if hkv % c == 0)  # 8 groups: 9.5 ms vs 18.3 serial at 32K
-        if hkv % chunks:
-            raise ConfigurationError(f"{hkv} kv heads cannot be cut into {chunks} chunks")
+            # two q heads per launch (a full CTA pair) when the group allows,
+            # at most 16 launches (l32k e2e: 16 groups 9.4 ms, 8 groups 9.5, serial 18.3)
+            qmin = 2 if grp % 2 == 0 else grp
+            chunks = max(c for c in range(1, min(16, hq // qmin) + 1) if valid(c))
+        if chunks < 1 or not valid(chunks):
+            raise ConfigurationError(f"{hq} q heads ({hkv} kv heads) cannot be cut into {chunks} chunks")
         dev = self.device
         if getattr(self, "_host_bufs", None) is None:
             self._host_bufs = (torch.empty(self.shape_q, dtype=torch.bfloat16, device=dev),
                                torch.empty(self.shape_kv, dtype=torch.bfloat16, device=dev),
                                torch.empty(self.shape_kv, dtype=torch.bfloat16, device=dev))
-            self._streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            self._streams = tuple(torch.cuda.Stream(dev) for _ in range(4))
         qd, kd, vd = self._host_bufs
-        s_in, s_out = self._streams
-        compute = torch.cuda.current_stream(dev)
-        kv_per, q_per = hkv // chunks, hq // chunks
+        s_in, s_out, c0, c1 = self._streams
+        current = torch.cuda.current_stream(dev)
+        q_per = hq // chunks
         self.counters.zero_()
         start = torch.cuda.Event()
-        start.record(compute)
-        s_in.wait_event(start)
-        s_out.wait_event(start)
+        start.record(current)
+        for st in self._streams:
+            st.wait_event(start)
         base = self.args
+        kv_copied = 0
         for c in range(chunks):
-            g0, h0 = c * kv_per, c * q_per
+            h0 = c * q_per
+            g0, g1 = h0 // grp, (h0 + q_per - 1) // grp + 1
             with torch.cuda.stream(s_in):
                 qd[:, h0:h0 + q_per].copy_(q_h[:, h0:h0 + q_per], non_blocking=True)
-                kd[:, g0:g0 + kv_per].copy_(k_h[:, g0:g0 + kv_per], non_blocking=True)
-                vd[:, g0:g0 + kv_per].copy_(v_h[:, g0:g0 + kv_per], non_blocking=True)
+                if g1 > kv_copied:
+                    kd[:, kv_copied:g1].copy_(k_h[:, kv_copied:g1], non_blocking=True)
+                    vd[:, kv_copied:g1].copy_(v_h[:, kv_copied:g1], non_blocking=True)
+                    kv_copied = g1
                 ready = torch.cuda.Event()
                 ready.record(s_in)
+            compute = c0 if c % 2 == 0 else c1
             compute.wait_event(ready)
             for bi in range(bsz):  # one launch per batch element: LSE / trace rows stay [b, h] addressed
                 a = _lib.FwdArgs.from_buffer_copy(base)
@@ -418,7 +435,7 @@ class BsfaPlan:
                 a.v_stride_b, a.v_stride_h, a.v_stride_n = vd.stride(0), vd.stride(1), vd.stride(2)
                 a.o = self.o[bi, h0].data_ptr()
                 a.lse = self.lse[bi, h0].data_ptr()
-                a.batch, a.heads_q, a.heads_kv = 1, q_per, kv_per
+                a.batch, a.heads_q, a.heads_kv = 1, q_per, g1 - g0
                 if self.thr is not None:
                     a.thresholds = self.thr[h0].data_ptr()
                 if self.decisions is not None:
@@ -429,7 +446,8 @@ class BsfaPlan:
             s_out.wait_event(done)
             with torch.cuda.stream(s_out):
                 o_h[:, h0:h0 + q_per].copy_(self.o[:, h0:h0 + q_per], non_blocking=True)
+        # s_out follows every kernel (it waited on each); the caller's stream follows s_out
         self.done = torch.cuda.Event()
         self.done.record(s_out)
-        compute.wait_event(self.done)
+        current.wait_event(self.done)
         return o_h

@@ -508,10 +508,11 @@ def test_online_rescale_path(bsfa, d):
         np.testing.assert_allclose(out.logsumexp, lse_ref, atol=1e-2)
 
 
-@pytest.mark.parametrize("B,hq,hkv,chunks", [(1, 8, 4, 4), (2, 8, 4, 2), (1, 4, 4, 4), (2, 6, 2, 1)])
+@pytest.mark.parametrize("B,hq,hkv,chunks", [(1, 8, 4, 4), (2, 8, 4, 2), (1, 4, 4, 4), (2, 6, 2, 1),
+                                             (1, 8, 2, 4), (2, 8, 2, None), (1, 6, 2, 2), (1, 8, 4, 8)])
 def test_plan_run_host_matches_device_run(bsfa, B, hq, hkv, chunks):
     """The pipelined host path (per kv-head group H2D | kernel | D2H) is the device launch, bit for bit."""
-    rng = np.random.default_rng(B * 100 + hq * 10 + chunks)
+    rng = np.random.default_rng(B * 100 + hq * 10 + (chunks or 0))
     n, d = 2048, 128
     q = torch.from_numpy(rng.standard_normal((B, hq, n, d)).astype(np.float32)).to(torch.bfloat16)
     k = torch.from_numpy(rng.standard_normal((B, hkv, n, d)).astype(np.float32)).to(torch.bfloat16)
@@ -532,7 +533,7 @@ def test_plan_run_host_matches_device_run(bsfa, B, hq, hkv, chunks):
     assert torch.equal(plan.counters[:2], cnt_dev[:2])
     assert 0 < int(cnt_dev[1]) < int(cnt_dev[0])
     with pytest.raises(bsfa.ConfigurationError):
-        plan.run_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, chunks=3)
+        plan.run_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, chunks=5)
 
 
 def test_calibrate_from_dump_directory(bsfa, tmp_path):
