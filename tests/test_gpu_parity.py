@@ -448,22 +448,27 @@ def test_threshold_file_round_trip_gpu_tensor(bsfa, tmp_path):
 
 
 # ------------------------------------------------------------------ full size (sampled heads)
-@pytest.mark.parametrize("n", [32768])
-def test_llama_shape_sampled_heads(bsfa, n):
-    """L32K Llama-3.1-8B shape (32 q / 8 kv heads, d=128): dense and ~50% skip, two heads checked."""
-    gen = torch.Generator(device="cuda").manual_seed(0)
-    q = torch.randn((1, 32, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
-    k = torch.randn((1, 8, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
-    v = torch.randn((1, 8, n, 128), generator=gen, device="cuda").to(torch.bfloat16)
-    T = 3.84
+@pytest.mark.parametrize("n,d,causal,b_n,T,heads", [
+    (32768, 128, True, 64, 3.84, (0, 29)),      # BASELINE configs[1]
+    (16384, 128, False, 64, 3.84, (5,)),        # non-causal: every off-tile gated
+    (16384, 64, True, 128, 4.1, (10,)),         # d = 64 kernel, 128x128 tiles
+    (65536, 128, True, 64, 3.84, (17,)),        # configs[2] length
+])
+def test_llama_shape_sampled_heads(bsfa, n, d, causal, b_n, T, heads):
+    """Llama-3.1-8B head layout (32 q / 8 kv heads): dense and ~50% skip, sampled heads vs the oracle."""
+    gen = torch.Generator(device="cuda").manual_seed(n + d)
+    q = torch.randn((1, 32, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, 8, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, 8, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tiles = bsfa.TileConfig(128, b_n)
     t = bsfa.ThresholdTensor(values=np.full((1, 1, 32, n // 128), T, dtype=np.float32), k_levels=(1,),
-                             n_max=n, b_m=128, b_n=64)
-    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True)
-    dense = bsfa.attention(q, k, v, return_trace=False)
+                             n_max=n, b_m=128, b_n=b_n)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True, causal=causal, tiles=tiles)
+    dense = bsfa.attention(q, k, v, return_trace=False, causal=causal, tiles=tiles)
     cnt = res.counters.cpu().numpy()
     skip = 1 - (cnt[1] - 0) / cnt[0]
-    assert 0.2 < skip < 0.7
-    for h in (0, 29):
+    assert 0.2 < skip < 0.8, skip
+    for h in heads:
         qh = q[0, h].float().cpu().numpy()
         kh = k[0, h // 4].float().cpu().numpy()
         vh = v[0, h // 4].float().cpu().numpy()
@@ -473,14 +478,14 @@ def test_llama_shape_sampled_heads(bsfa, n):
         def keep_fn(i_idx, j, smax):
             return dec[i_idx, j] == orc.KEPT
 
-        o_ref, _, dec_ref = orc.flash_forward_fast(qh, kh, vh, True, 128, 64, keep_fn, record=rec)
+        o_ref, _, dec_ref = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n, keep_fn, record=rec)
         # mask parity: the GPU decision must agree with T on every tile away from the threshold
         for j, (i_idx, smax) in rec.items():
             far = np.abs(smax - T) > EPS
             want = np.where(smax > T, orc.KEPT, orc.SKIPPED)
             assert (dec[i_idx[far], j] == want[far]).all(), (h, j)
         assert np.abs(res.o[0, h].float().cpu().numpy() - o_ref).max() <= ATOL
-        od_ref, _, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+        od_ref, _, _ = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n,
                                               lambda i_idx, j, sm: np.ones(len(i_idx), bool))
         assert np.abs(dense.o[0, h].float().cpu().numpy() - od_ref).max() <= ATOL
 
