@@ -61,10 +61,6 @@
 #ifndef BSFA_P_SMEM
 #define BSFA_P_SMEM 1
 #endif
-// Load the score row in two halves and reduce the first while the second loads.
-#ifndef BSFA_SPLIT_LD
-#define BSFA_SPLIT_LD 0
-#endif
 // Debug timeline (bsfa_debug_trace); compiled out of the production library.
 #ifndef BSFA_TRACE
 #define BSFA_TRACE 0
@@ -852,43 +848,28 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       if (tr0 && j < kTraceSteps) p.trace[(kEvSReady * 2 + s) * kTraceSteps + j] = clock64();
       tc_fence_after();
       uint32_t sv[128];
-#if BSFA_SPLIT_LD
-      // keys 64-127 load while the first half is masked and reduced
-      tmem_ld32(s_row, &sv[0]);
-      tmem_ld32(s_row + 32, &sv[32]);
-      tmem_wait_ld();
-      tmem_ld32(s_row + 64, &sv[64]);
-      tmem_ld32(s_row + 96, &sv[96]);
-#else
 #pragma unroll
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
-#endif
 
       const int sb = CALIB ? -1 : step_static_bits<GT>(gate_mode, window, j, qi);
-      // row max per 64-key half (three-input FMNMX, four chains each), after
-      // the frontier / padded-key masks
+      if (!CALIB) {
+        if (j == qi && causal) {  // frontier step: key offset c vs row r inside block i
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c > r) sv[c] = __float_as_uint(-INFINITY);
+        }
+        if (!causal && (j + 1) * 128 > valid_len) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (j * 128 + c >= valid_len) sv[c] = __float_as_uint(-INFINITY);
+        }
+      }
+      // row max per 64-key half (three-input FMNMX, four chains each)
       float mh[2];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t* x = sv + hh * 64;
-        if (BSFA_SPLIT_LD && hh == 1) {
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 64; ++c) asm volatile("" : "+r"(x[c]));  // no use may move above the wait
-        }
-        if (!CALIB) {
-          if (j == qi && causal) {  // frontier step: key offset c vs row r inside block i
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (hh * 64 + c > r) x[c] = __float_as_uint(-INFINITY);
-          }
-          if (!causal && (j + 1) * 128 > valid_len) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (j * 128 + hh * 64 + c >= valid_len) x[c] = __float_as_uint(-INFINITY);
-          }
-        }
+        const uint32_t* x = sv + hh * 64;
         float a0 = fmax3(__uint_as_float(x[0]), __uint_as_float(x[1]), __uint_as_float(x[2]));
         float a1 = fmax3(__uint_as_float(x[3]), __uint_as_float(x[4]), __uint_as_float(x[5]));
         float a2 = fmax3(__uint_as_float(x[6]), __uint_as_float(x[7]), __uint_as_float(x[8]));

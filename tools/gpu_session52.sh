@@ -1,0 +1,9 @@
+# current default (per-half mask+max loop) vs the s48 build: A/B x3 on one box
+V=$PWD/paper_2512_07011_b200/_lib/variants
+for i in 1 2 3; do
+  for t in default s48; do
+    if [ $t = default ]; then unset BSFA_LIB_PATH; else export BSFA_LIB_PATH=$V/libbsfa_b200_$t.so; fi
+    timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/b52_$t.json 2>gpurun_out/b52_$t.err
+    python -c "import json; d=json.load(open('gpurun_out/b52_$t.json')); print('$t', round(d['ms_per_step'],3), round(d['value'],1), round(d['dense_ms_per_step'],3), round(d['dense_tflops'],1), round(d['speedup_vs_dense'],3))" || tail -3 gpurun_out/b52_$t.err
+  done
+done
