@@ -104,15 +104,22 @@ class CalibrationDiagnostics:
 
 
 def _head_operand(x, n_pad: int, d_pad: int, device) -> torch.Tensor:
-    """[H, N, d] numpy/torch -> bf16 [H, n_pad, d_pad] on `device` (rows repeated, d zero-padded)."""
+    """[H, N, d] numpy/torch -> bf16 [H, n_pad, d_pad] on `device` (rows repeated, d zero-padded).
+
+    A bf16 device tensor of the padded shape with 16-byte aligned rows is used
+    as is (no copy); anything else is rounded to bf16 once (RNE, as the
+    forward does) and padded.
+    """
     t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
-    t = t.to(device=device, dtype=torch.float32, non_blocking=True)
+    t = t.to(device=device, non_blocking=True).to(torch.bfloat16)
     n = t.shape[1]
     if n != n_pad:
         t = torch.cat([t, t[:, n - 1:n].expand(-1, n_pad - n, -1)], dim=1)
     if t.shape[2] != d_pad:
         t = torch.nn.functional.pad(t, (0, d_pad - t.shape[2]))
-    return t.to(torch.bfloat16).contiguous()
+    if t.stride(2) != 1 or (t.stride(1) * 2) % 16 or (t.stride(0) * 2) % 16 or t.data_ptr() % 16:
+        t = t.contiguous()
+    return t
 
 
 class Calibrator:

@@ -171,7 +171,8 @@ struct KCfg {
   // TMEM columns
   static constexpr int O_COL = 0;                          // O_s at s * D
   static constexpr int S_COL = CALIB ? 0 : NQ * D;         // S_s at S_COL + s * 128
-  static constexpr int TMEM_NEED = S_COL + NQ * 128;
+  // calibration has no O: S is double-buffered per query tile, S_{s,b} at (2s + b) * 128
+  static constexpr int TMEM_NEED = CALIB ? NQ * 256 : S_COL + NQ * 128;
   static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
   // one thread per row: warpgroup s is query tile s; the last warpgroup holds
   // the K producer, the MMA issuer, the V producer and one idle warp
@@ -415,14 +416,29 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         const int st = j % KS;
         if (s == 0) mbar_wait((k_full + 8 * (st)), (j / KS) & 1);
         tc_fence_after();
-        umma_qk_tile_w<D, 128>(tmem + C::S_COL + s * 128, dq0 + uint64_t((s * C::Q_TILE) >> 4),
+        // calibration: buffer j & 1, completion on s_full (b = 0) or the unused o_full slot (b = 1)
+        const uint32_t d_tmem = CALIB ? tmem + (2 * s + (j & 1)) * 128 : tmem + C::S_COL + s * 128;
+        umma_qk_tile_w<D, 128>(d_tmem, dq0 + uint64_t((s * C::Q_TILE) >> 4),
                                dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
         if (s == NQ - 1) umma_commit_w((k_empty + 8 * (st)));
-        umma_commit_w((s_full + 8 * (s)));
+        umma_commit_w(CALIB && (j & 1) ? (o_full + 8 * (s)) : (s_full + 8 * (s)));
       };
 
 #pragma unroll
       for (int s = 0; s < NQ; ++s) issue_qk(s, 0);
+      if constexpr (CALIB) {
+        // QK_s(j+2) goes into the buffer the softmax released for step j
+        if (nsteps > 1)
+#pragma unroll
+          for (int s = 0; s < NQ; ++s) issue_qk(s, 1);
+        for (int j = 0; j + 2 < nsteps; ++j) {
+#pragma unroll
+          for (int s = 0; s < NQ; ++s) {
+            mbar_wait((p_full + 8 * (2 * s + (j & 1))), (j >> 1) & 1);
+            issue_qk(s, j + 2);
+          }
+        }
+      }
 
       unsigned vbase = 0;      // V units consumed before this step
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
@@ -475,7 +491,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           for (unsigned x = 0; x < nunits; ++x) umma_commit_w((v_empty + 8 * ((vbase + x) % VS)));
           vbase += nunits;
         }
-      } else {
+      } else if constexpr (!CALIB) {
       for (int j = 0; j < nsteps; ++j) {
         const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
         uint32_t prev = 0;     // gate tiles already assigned a V slot this step
@@ -844,12 +860,16 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     };
     for (int j = 0; j < nsteps; ++j) {
       if (BSFA_TURN == 2) turn_wait(j);
-      mbar_wait((s_full + 8 * (s)), j & 1);
+      if constexpr (CALIB)
+        mbar_wait((j & 1) ? (o_full + 8 * (s)) : (s_full + 8 * (s)), (j >> 1) & 1);
+      else
+        mbar_wait((s_full + 8 * (s)), j & 1);
       if (tr0 && j < kTraceSteps) p.trace[(kEvSReady * 2 + s) * kTraceSteps + j] = clock64();
       tc_fence_after();
       uint32_t sv[128];
+      const uint32_t s_buf = CALIB ? tmem + lane_off + (2 * s + (j & 1)) * 128 : s_row;
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
+      for (int c = 0; c < 128; c += 32) tmem_ld32(s_buf + c, &sv[c]);
       tmem_wait_ld();
 
       const int sb = CALIB ? -1 : step_static_bits<GT>(gate_mode, window, j, qi);
@@ -897,17 +917,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       if constexpr (CALIB) {
 #pragma unroll
         for (int x = 0; x < GT; ++x) {
-          float m = mx[x];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-          if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * GT + x], float_to_ordered(m * scale));
+          // warp max in one REDUX on the order-preserving integer image of the scaled max
+          const int m = __reduce_max_sync(0xffffffffu, float_to_ordered(mx[x] * scale));
+          if (lane == 0) atomicMax(&cvals[s * C::MAXA + j * GT + x], m);
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive((p_half + 8 * (0)));
-          mbar_arrive((p_half + 8 * (1)));
-        }
+        if (lane == 0) mbar_arrive((p_half + 8 * (j & 1)));  // buffer j & 1 may take QK_s(j+2)
         continue;
       } else {
         // ---- gate decision; votes are OR-reduced over the tile's 128 rows in the
