@@ -416,14 +416,14 @@ def main():
         h2d = qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2
         d2h = oh.numel() * 2
 
-        def e2e_step():  # kv-head groups pipelined: H2D(c+1) | kernel(c) | D2H(c-1)
+        def e2e_step():  # q-head groups pipelined: H2D(c+1) | kernel(c) | D2H(c-1)
             plan.run_host(qh, kh, vh, oh, chunks=args.e2e_chunks)
 
         et, etot = time_steps(e2e_step, max(3, args.steps // 2), 2, stream)
         ems = max_over_ranks(etot / max(3, args.steps // 2), world)
         e2e = {"value": job_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "pipeline": "kv-head groups: H2D(c+1) | kernel(c) | D2H(c-1) on three streams"}
+               "pipeline": "q-head groups: H2D(c+1) | kernel(c) | D2H(c-1); copy, two compute and copy-back streams"}
 
     peak, peak_sus, peak_src = measured_peaks()
     achieved = f_exec / (mean_launch_ms * 1e-3) / 1e12

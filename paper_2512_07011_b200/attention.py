@@ -436,6 +436,7 @@ class BsfaPlan:
                 a.o = self.o[bi, h0].data_ptr()
                 a.lse = self.lse[bi, h0].data_ptr()
                 a.batch, a.heads_q, a.heads_kv = 1, q_per, g1 - g0
+                a.num_o_peers = 0  # the host path returns O to the host; no peer copies
                 if self.thr is not None:
                     a.thresholds = self.thr[h0].data_ptr()
                 if self.decisions is not None:
