@@ -157,10 +157,18 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BSFA_BENCH_ONE_DEVICE=1 (+ BSFA_BENCH_BACKEND=gloo): every rank on cuda:0 -- only for
+    # exercising the multi-rank code path on a one-GPU box; numbers from such a run are not scaling data
+    if os.environ.get("BSFA_BENCH_ONE_DEVICE") == "1":
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BSFA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return rank, world, local
