@@ -9,6 +9,10 @@
 
 #include "../../include/bsfa_b200.h"
 #include "bsfa_kernel.cuh"
+// forward at b_n = 64, d = 128, GQA groups of 4k: the CTA-pair kernel (bsfa_kernel_pair.cuh)
+#ifndef BSFA_PAIR
+#define BSFA_PAIR 0
+#endif
 // forward at b_n = 64: the Q-in-TMEM 64-key-step kernel (bsfa_kernel_qt.cuh)
 #ifndef BSFA_QT_FWD
 #define BSFA_QT_FWD 0
@@ -18,6 +22,7 @@
 #endif
 #include "bsfa_kernel_gs.cuh"
 #include "bsfa_kernel_qt.cuh"
+#include "bsfa_kernel_pair.cuh"
 
 static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
 
@@ -125,6 +130,24 @@ int launch_gs(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& t
   if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
   return BSFA_OK;
 }
+
+int launch_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p,
+                int units, cudaStream_t st) {
+  using C = PairCfg;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(bsfa_kernel_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  if (units == 0) return BSFA_OK;
+  bsfa_kernel_pair<<<2 * units, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa pair kernel launch");
+  return BSFA_OK;
+}
+
+bool use_pair(int d, int b_n, int group) { return BSFA_PAIR && d == 128 && b_n == 64 && group % 4 == 0; }
 
 template <int D, int NQ>
 int launch_qt(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
@@ -253,7 +276,11 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
-                       ((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64) ? 64 : 128, "k"))
+                       (((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64) ||
+                        use_pair(a->head_dim, a->b_n, a->heads_q / a->heads_kv))
+                           ? 64
+                           : 128,
+                       "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))
@@ -299,6 +326,11 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.counters = a->counters;
   p.status = a->status;
 
+  if (use_pair(d, a->b_n, p.group)) {
+    const long long units = (long long)a->batch * (a->heads_q / 4) * p.num_q_tiles;
+    if (2 * units > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
+    return launch_pair(tq, tk, tv, p, (int)units, reinterpret_cast<cudaStream_t>(stream));
+  }
   const int nq = tiles_per_cta(p.group);
   const long long grid = (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
