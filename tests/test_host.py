@@ -221,3 +221,27 @@ def test_calibration_argument_validation():
         bsfa.CalibrationDump(2, 1, 16, [s])
     with pytest.raises(InvalidInputError):
         bsfa.CalibrationSample(0, np.zeros((1, 3, 8, 4)), np.zeros((1, 2, 8, 4)))
+
+
+def test_struct_offsets_match_the_c_compiler(tmp_path):
+    """Byte layout of the ctypes mirrors == what a C compiler makes of include/bsfa_b200.h."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "bsfa_b200.h"', "int main(void) {"]
+    for cname, cls in (("bsfa_fwd_args", _lib.FwdArgs), ("bsfa_calib_args", _lib.CalibArgs)):
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{cname}.{f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = dict(line.rsplit(" ", 1) for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                              check=True).stdout.splitlines())
+    for cname, cls in (("bsfa_fwd_args", _lib.FwdArgs), ("bsfa_calib_args", _lib.CalibArgs)):
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for f in cls._fields_:
+            assert int(got[f"{cname}.{f[0]}"]) == getattr(cls, f[0]).offset, (cname, f[0])
