@@ -240,6 +240,17 @@ def time_steps(fn, steps, warmup, stream):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_port(cfg, tiles, T_slice, seconds_budget=20.0):
     """Oracle port of the reference engine (engine.py:117-193) on one host core.
 
@@ -272,7 +283,7 @@ def cpu_baseline_port(cfg, tiles, T_slice, seconds_budget=20.0):
             i -= 1
     dt = time.perf_counter() - t0
     fl = costs.executed_flops(reach, kept, tiles, d)
-    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "cpu": cpu_model(), "kind": "port",
             "sample": f"head 0, last {done_blocks} of {m_q} query blocks ({reach} tiles) of the {n}-token "
                       f"workload, threshold gate, numpy oracle port, 1 thread, {dt:.1f} s"}
 
@@ -329,7 +340,8 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": args.config, **cfg, "tiles": "128x64", "causal": True},
-            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "cpu": cpu_model(), "kind": "port",
+                             "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
