@@ -61,6 +61,12 @@
 #ifndef BSFA_P_SMEM
 #define BSFA_P_SMEM 1
 #endif
+// One tcgen05 issuer warp per query tile (the otherwise idle warp issues for
+// tile 1), V in fixed slots per (step, gate tile): a tile's MMAs never wait
+// behind the other tile's barriers.
+#ifndef BSFA_SPLIT_ISSUE
+#define BSFA_SPLIT_ISSUE 0
+#endif
 // Debug timeline (bsfa_debug_trace); compiled out of the production library.
 #ifndef BSFA_TRACE
 #define BSFA_TRACE 0
@@ -145,6 +151,7 @@ struct KCfg {
   static constexpr bool PSM = !CALIB && TPR == 1 && BSFA_P_SMEM != 0;
   static constexpr int P_TILE = PSM ? 128 * 128 : 0;  // 128 rows x 64 keys bf16 per query tile
   static constexpr int KS = D == 128 ? (PSM ? 2 : BSFA_K_STAGES) : 3;
+  static constexpr bool SPLIT = PSM && BSFA_SPLIT_ISSUE != 0;  // one issuer warp per query tile
   static constexpr int VS = CALIB ? 0 : (D == 128 ? BSFA_V_BYTES : 65536) / V_UNIT;
 #ifndef BSFA_DQ
 #define BSFA_DQ 4
@@ -287,11 +294,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     mbar_init(bar_q, 1);
     for (int i = 0; i < KS; ++i) {
       mbar_init((k_full + 8 * (i)), 1);
-      mbar_init((k_empty + 8 * (i)), 1);
+      mbar_init((k_empty + 8 * (i)), C::SPLIT ? NQ : 1);
     }
     for (int i = 0; i < VS; ++i) {
       mbar_init((v_full + 8 * (i)), 1);
-      mbar_init((v_empty + 8 * (i)), 1);
+      mbar_init((v_empty + 8 * (i)), C::SPLIT ? NQ : 1);
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init((s_full + 8 * (s)), 1);
@@ -317,6 +324,73 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  // ---- split issue (C::SPLIT): the tcgen05 work of query tile s, issued by its own warp
+  auto split_issue = [&](int s) {
+    constexpr uint32_t IDESC_QK = make_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t IDESC_PV = make_idesc_bf16(128, D, 0, 1);
+    const uint64_t dq0 = make_sdesc_sw128(sQ, 16, 1024);
+    const uint64_t dk0 = make_sdesc_sw128(sK, 16, 1024);
+    const uint64_t dv0 = make_sdesc_sw128(sV, BN * 128, 1024);
+    const uint64_t dp0 = make_sdesc_sw128(sP, 16, 1024);
+    mbar_wait(bar_q, 0);
+    auto issue_qk = [&](int j) {
+      const int st = j % KS;
+      mbar_wait((k_full + 8 * (st)), (j / KS) & 1);
+      tc_fence_after();
+      umma_qk_tile_w<D, 128>(tmem + C::S_COL + s * 128, dq0 + uint64_t((s * C::Q_TILE) >> 4),
+                             dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
+      umma_commit_w((k_empty + 8 * (st)));  // one of NQ releases of the stage
+      umma_commit_w((s_full + 8 * (s)));
+    };
+    issue_qk(0);
+    uint32_t use_par = 0;  // bit slot: v_full phase (one phase per use of the slot)
+    uint32_t p1_par = 0;
+    bool o_started = false;
+    for (int j = 0; j < nsteps; ++j) {
+      const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
+      mbar_wait((p_full + 8 * (2 * s)), j & 1);
+      tc_fence_after();
+      const uint32_t bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + s * 4);
+      uint32_t rd = 0;  // gate tiles whose V this tile reads this step
+      if (bits & 1u) {
+        const int slot = (GT * j) % VS;
+        mbar_wait((v_full + 8 * (slot)), (use_par >> slot) & 1u);
+        tc_fence_after();
+        umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::S_COL + s * 128, dv0 + uint64_t((slot * C::V_UNIT) >> 4),
+                    IDESC_PV, o_started ? 1u : 0u);
+        o_started = true;
+        rd |= 1u;
+      }
+      if (j + 1 < nsteps) issue_qk(j + 1);  // S_s is free once P half 0 is consumed
+      constexpr int x1 = GT == 2 ? 1 : 0;
+      if ((bits >> x1) & 1u) {
+        mbar_wait((p_full + 8 * (2 * s + 1)), p1_par & 1u);  // released for kept second halves only
+        p1_par ^= 1u;
+        const int slot = (GT * j + x1) % VS;
+        if (GT == 2) mbar_wait((v_full + 8 * (slot)), (use_par >> slot) & 1u);
+        tc_fence_after();
+        umma_pv64_ss_w(tmem + C::O_COL + s * D, dp0 + uint64_t((s * C::P_TILE) >> 4),
+                       dv0 + uint64_t((slot * C::V_UNIT) >> 4) + uint64_t(GT == 1 ? 512 : 0), IDESC_PV,
+                       o_started ? 1u : 0u);
+        o_started = true;
+        rd |= 1u << x1;
+      }
+      umma_commit_w((pv_done + 8 * (s)));
+      if (j == nsteps - 1) umma_commit_w((o_full + 8 * (s)));
+      // hand this step's V slots back (after the producer announced them)
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        const int slot = (GT * j + h) % VS;
+        if ((rd >> h) & 1u) {
+          umma_commit_w((v_empty + 8 * (slot)));
+        } else {
+          mbar_wait((v_full + 8 * (slot)), (use_par >> slot) & 1u);
+          mbar_arrive_w((v_empty + 8 * (slot)));
+        }
+        use_par ^= 1u << slot;
+      }
+    }
+  };
   // Register split: setmaxnreg inside each role (the regions must not merge,
   // or ptxas allocates the merged code at the smaller budget).  Every role
   // leaves through bsfa_role_exit: arrive on the teardown barrier; the MMA
@@ -354,6 +428,52 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       if (nsteps > 0) {
         if (lane == 0) tma_prefetch_desc(&tm_v);
         unsigned vcount = 0, dn = 0;
+        if constexpr (C::SPLIT) {
+          // fixed slot per (step, gate tile); every use of a slot is announced on
+          // v_full (with the data, or empty), so both issuers track its phase alone
+          uint32_t use_par = 0;
+          auto use_slot = [&](int j, int h, bool load) {
+            const int slot = (GT * j + h) % VS;
+            mbar_wait((v_empty + 8 * (slot)), ((use_par >> slot) & 1u) ^ 1u);
+            use_par ^= 1u << slot;
+            if (load) {
+              mbar_arrive_expect_tx_w((v_full + 8 * (slot)), C::V_UNIT);
+#pragma unroll
+              for (int c = 0; c < C::NCH; ++c)
+                tma_load_4d_w(sV + slot * C::V_UNIT + c * BN * 128, &tm_v, (v_full + 8 * (slot)), c * 64,
+                              j * 128 + h * BN, g, b, kEvictLast);
+              ++vcount;
+            } else {
+              mbar_arrive_w((v_full + 8 * (slot)));
+            }
+          };
+          for (int j = 0; j < nsteps; ++j) {
+            const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
+            uint32_t done = 0;
+            if (sb >= 0) {
+#pragma unroll
+              for (int h = 0; h < GT; ++h) use_slot(j, h, (sb >> h) & 1);
+              continue;
+            }
+            const int di = int(dn % DQ);
+            const uint32_t ph = (dn / DQ) & 1;
+#pragma unroll
+            for (int s = 0; s < NQ; ++s) {
+              mbar_wait((dec_full + 8 * (s * DQ + di)), ph);
+              const uint32_t w = lds_u32(dec_sm + (s * DQ + di) * 4);
+              __syncwarp();
+              mbar_arrive_w((dec_empty + 8 * (s * DQ + di)));
+#pragma unroll
+              for (int h = 0; h < GT; ++h)
+                if (((w & ~done) >> h) & 1u) use_slot(j, h, true);
+              done |= w;
+            }
+#pragma unroll
+            for (int h = 0; h < GT; ++h)
+              if (!((done >> h) & 1u)) use_slot(j, h, false);
+            ++dn;
+          }
+        } else {
         auto load_unit = [&](int j, int h) {
           const int slot = int(vcount % VS);
           mbar_wait((v_empty + 8 * (slot)), ((vcount / VS) & 1) ^ 1);
@@ -390,6 +510,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
             ++dn;
           }
         }
+        }
         if (lane == 0 && p.counters) {
           atomicAdd(&p.counters[2], (unsigned long long)vcount);
           atomicAdd(&p.counters[3], (unsigned long long)nsteps * GT);
@@ -402,7 +523,9 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
   } else if (warp == C::MMA_WARP) {
     if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
     // ======================= MMA issuer (warp-convergent, one elected issuer) ==========
-    if (nsteps > 0) {
+    if (C::SPLIT && nsteps > 0) {
+      split_issue(0);
+    } else if (nsteps > 0) {
       constexpr uint32_t IDESC_QK = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t IDESC_PV = make_idesc_bf16(128, D, 0, 1);
       // descriptor templates; per-MMA offsets only touch the 14-bit start-address field
@@ -1191,8 +1314,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     named_bar_arrive(15, C::NUM_THREADS);
     return;
   } else {
-    // idle warp (completes the last warpgroup for setmaxnreg)
+    // idle warp (completes the last warpgroup for setmaxnreg); issues query
+    // tile 1's tcgen05 work in split-issue builds
     if constexpr (C::SPLIT_REGS) setmaxnreg_dec<C::REG_OTHER>();
+    if constexpr (C::SPLIT && NQ == 2) {
+      if (nsteps > 0) split_issue(1);
+      __syncwarp();
+    }
     named_bar_arrive(15, C::NUM_THREADS);
     return;
   }
