@@ -6,7 +6,9 @@ For each sequence length: thresholds calibrated on a separate synthetic sample
 (seed 1000) for each target predicted density (reference costs.predicted_density
 inverted to a k level), then BSFA and the same kernel with the DenseGate timed
 with CUDA events (inputs resident, 32 q / 8 kv heads, d=128, causal, 128x64
-tiles).  One JSON line per (seq, density) plus one dense line per seq.
+tiles).  One JSON line per (seq, density) plus one dense line per seq; each
+speedup divides by a dense run timed right after the BSFA run (a first, cold
+dense run is up to 10 % faster than later ones).
 """
 import argparse
 import json
@@ -45,13 +47,15 @@ def main():
         f_dense = costs.dense_flops(int(cnt[0]), tiles, 128)
         print(json.dumps({"seq_len": n, "gate": "dense", "ms": dms, "tflops": f_dense / dms / 1e9,
                           "frac_of_peak": f_dense / dms / 1e9 / peak, "peak_source": src}), flush=True)
-        del dplan
         for dens in args.densities:
             kl = costs.k_for_density(n, tiles, dens)
             thr = bench.calibrated_thresholds(cfg, tiles, kl, dev)
             plan = bsfa.BsfaPlan(1, 32, 8, n, 128, tiles=tiles, thresholds=thr, k_level=kl, device=dev)
             _, tot = bench.time_steps(lambda: plan.run(q, k, v), args.steps, args.warmup, stream)
             ms = tot / args.steps
+            # dense again right after, so the speedup pairs runs at the same thermal state
+            _, dtot2 = bench.time_steps(lambda: dplan.run(q, k, v), args.steps, 1, stream)
+            dms_pair = dtot2 / args.steps
             c = plan.counters.cpu().numpy()
             reach, kept, vl, vu = (int(x) for x in c)
             f_exec = costs.executed_flops(reach, kept, tiles, 128)
@@ -59,8 +63,10 @@ def main():
                               "measured_density": kept / reach, "skip_frac": 1 - kept / reach,
                               "v_fetch_skip_frac": 1 - vl / vu, "ms": ms, "exec_tflops": f_exec / ms / 1e9,
                               "effective_dense_tflops": costs.dense_flops(reach, tiles, 128) / ms / 1e9,
-                              "frac_of_peak": f_exec / ms / 1e9 / peak, "speedup_vs_dense": dms / ms}), flush=True)
+                              "frac_of_peak": f_exec / ms / 1e9 / peak, "dense_ms_adjacent": dms_pair,
+                              "speedup_vs_dense": dms_pair / ms}), flush=True)
             del plan, thr
+        del dplan
         del q, k, v
         torch.cuda.empty_cache()
 
