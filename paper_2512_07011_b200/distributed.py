@@ -170,3 +170,54 @@ def sharded_attention(q, k, v, *, rank: int, world: int, thresholds=None, layer:
     if gather:
         return res, gather_heads(res.o, world, group)
     return res, None
+
+
+def sharded_calibrate(dump, k_levels, tiles, *, rank: int, world: int, group=None, calibrate_fn=None):
+    """Threshold calibration sharded like the forward: rank r
+    calibrates the q heads of its kv-head groups over every layer and sample,
+    then the per-rank [S, L, H/W, P] slices are all-gathered into the full
+    ThresholdTensor -- identical on every rank to a single-process calibrate().
+
+    ``calibrate_fn(dump, k_levels, tiles)`` defaults to the GPU
+    :func:`~paper_2512_07011_b200.calibration.calibrate`; tests substitute a
+    CPU checker to exercise the partition and gather on gloo.
+    """
+    import numpy as np
+
+    from .calibration import CalibrationDiagnostics, CalibrationDump, CalibrationSample, calibrate
+    from .thresholds import ThresholdTensor
+
+    calibrate_fn = calibrate_fn or calibrate
+    if not dump.samples:
+        raise ConfigurationError("calibration dump has no samples")
+    hq, hkv = dump.samples[0].q.shape[1], dump.samples[0].k.shape[1]
+    sh = shard_heads(hq, hkv, world, rank)
+    local = CalibrationDump(dump.num_layers, sh.num_q, dump.head_dim, [
+        CalibrationSample(s.sample_id, s.q[:, sh.q_lo:sh.q_hi], s.k[:, sh.kv_lo:sh.kv_hi]) for s in dump.samples])
+    part = calibrate_fn(local, k_levels, tiles)
+    if world == 1:
+        return part
+    vals = torch.from_numpy(np.ascontiguousarray(part.values))
+    dev = None
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        vals = vals.to(dev)
+    out = [torch.empty_like(vals) for _ in range(world)]
+    dist.all_gather(out, vals, group=group)
+    values = torch.cat(out, dim=2).cpu().numpy()  # ranks own consecutive head ranges
+    ties = {}
+    if getattr(part, "diagnostics", None) is not None:
+        local_ties = torch.tensor([part.diagnostics.tie_counts[k] for k in part.k_levels], dtype=torch.int64,
+                                  device=dev)
+        dist.all_reduce(local_ties, group=group)
+        ties = {k: int(v) for k, v in zip(part.k_levels, local_ties.cpu().tolist())}
+        stats = {}
+        for si, k in enumerate(part.k_levels):
+            fv = values[si][np.isfinite(values[si])]
+            stats[k] = (float(fv.min()), float(fv.mean()), float(fv.max())) if fv.size else (None, None, None)
+        diag = CalibrationDiagnostics(num_samples=part.diagnostics.num_samples, tie_counts=ties,
+                                      threshold_stats=stats)
+    else:
+        diag = None
+    return ThresholdTensor(values=values, k_levels=part.k_levels, n_max=part.n_max, b_m=part.b_m, b_n=part.b_n,
+                           diagnostics=diag)

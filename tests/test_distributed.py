@@ -151,3 +151,49 @@ def test_two_rank_peer_gather(batch):
     for rank, shape, err in results:
         assert shape == (batch, hq, n, d)
         assert err == 0.0, (rank, err)
+
+
+def _oracle_calibrate(dump, k_levels, tiles):
+    """CPU stand-in for the GPU calibrate(): the oracle restatement (calibration.py:156-222)."""
+    import paper_2512_07011_b200 as bsfa
+    from oracle import bsfa_oracle as orc
+    samples = [(s.sample_id, np.asarray(s.q), np.asarray(s.k)) for s in dump.samples]
+    values, n_max, _ = orc.calibrate(samples, k_levels, tiles.b_m, tiles.b_n)
+    return bsfa.ThresholdTensor(values=values, k_levels=tuple(k_levels), n_max=n_max, b_m=tiles.b_m, b_n=tiles.b_n)
+
+
+def _calib_worker(rank, world, port, dump, result_q):
+    import paper_2512_07011_b200 as bsfa
+    from paper_2512_07011_b200.distributed import sharded_calibrate
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = sharded_calibrate(dump, [1, 3], bsfa.TileConfig(128, 64), rank=rank, world=world,
+                              calibrate_fn=_oracle_calibrate)
+        result_q.put((rank, t.values))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_calibration_matches_single_process():
+    import paper_2512_07011_b200 as bsfa
+    from oracle import bsfa_oracle as orc
+    rng = np.random.default_rng(3)
+    L, hq, hkv, n, d = 2, 4, 2, 512, 16
+    samples = [bsfa.CalibrationSample(sid, orc.round_bf16(rng.standard_normal((L, hq, n, d)).astype(np.float32)),
+                                      orc.round_bf16(rng.standard_normal((L, hkv, n, d)).astype(np.float32)))
+               for sid in (0, 1)]
+    dump = bsfa.CalibrationDump(L, hq, d, samples)
+    want = _oracle_calibrate(dump, [1, 3], bsfa.TileConfig(128, 64)).values
+    ctx = mp.get_context("spawn")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_calib_worker, args=(r, 2, port, dump, result_q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    results = sorted((result_q.get(timeout=10) for _ in range(2)), key=lambda x: x[0])
+    for rank, values in results:
+        np.testing.assert_array_equal(values, want)
