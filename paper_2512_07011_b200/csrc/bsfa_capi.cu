@@ -331,8 +331,14 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
     if (2 * units > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
     return launch_pair(tq, tk, tv, p, (int)units, reinterpret_cast<cudaStream_t>(stream));
   }
-  const int nq = tiles_per_cta(p.group);
-  const long long grid = (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
+  // odd GQA groups (MHA included): two query blocks of one q head per CTA, so the
+  // two-tile pipeline still runs (main kernel, one thread per row, second-half P
+  // in shared memory)
+  const bool main_path = !((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64);
+  p.block_pair = (p.group % 2 == 1 && main_path && BSFA_TPR == 1 && BSFA_P_SMEM && !BSFA_SPLIT_ISSUE) ? 1 : 0;
+  const int nq = p.block_pair ? 2 : tiles_per_cta(p.group);
+  const long long grid = p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
+                                      : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
   return dispatch<false>(d, a->b_n, nq, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -113,6 +113,9 @@ struct KernelParams {
   // debug: per-step clock64 timestamps of one CTA (bsfa_debug_trace)
   long long* trace;
   int trace_cta;
+  // NQ = 2 forward with an odd GQA group (or MHA): the two query tiles are query
+  // blocks 2m+1 and 2m of ONE q head instead of two q heads of one block
+  int block_pair;
   // extra O destinations (peer GPUs' gathered-O buffers), same element offsets
   int num_o_peers;
   __nv_bfloat16* o_peer[7];
@@ -270,19 +273,50 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 
   // ---- work unit: (batch, kv head) major, heaviest query block first, the
   //      head pairs of the GQA group minor (every pair reads the same K/V)
-  const int pairs = p.group / NQ;
-  const int per_bg = p.num_q_tiles * pairs;
-  const int unit = blockIdx.x;
-  const int bg = unit / per_bg;
-  const int rem = unit - bg * per_bg;
-  const int qi = p.num_q_tiles - 1 - rem / pairs;
-  const int pr = rem - (rem / pairs) * pairs;
-  const int b = bg / p.heads_kv;
-  const int g = bg - b * p.heads_kv;
-  const int hq0 = g * p.group + pr * NQ;  // q head of query tile s = hq0 + s
+  // per query tile s: query block qi_a[s], q head hq_a[s], steps ns_a[s]
+  const bool bpair = !CALIB && NQ == 2 && p.block_pair != 0;
+  int qi_a[NQ], hq_a[NQ], ns_a[NQ];
+  int b_, g_, qi_, hq0_;
+  {
+    const int unit = blockIdx.x;
+    if (bpair) {
+      // query blocks 2m+1 and 2m of one q head (heaviest first); they share K/V
+      // up to the shorter tile's frontier, tile 1 simply stops one step earlier
+      const int per_bg = ((p.num_q_tiles + 1) / 2) * p.group;
+      const int bg = unit / per_bg;
+      const int rem = unit - bg * per_bg;
+      const int m = rem / p.group;
+      b_ = bg / p.heads_kv;
+      g_ = bg - b_ * p.heads_kv;
+      qi_ = p.num_q_tiles - 1 - 2 * m;
+      hq0_ = g_ * p.group + (rem - m * p.group);
+      qi_a[0] = qi_;
+      qi_a[NQ - 1] = qi_ - 1;  // -1: no second block (odd block count)
+      hq_a[0] = hq_a[NQ - 1] = hq0_;
+    } else {
+      const int pairs = p.group / NQ;
+      const int per_bg = p.num_q_tiles * pairs;
+      const int bg = unit / per_bg;
+      const int rem = unit - bg * per_bg;
+      qi_ = p.num_q_tiles - 1 - rem / pairs;
+      const int pr = rem - (rem / pairs) * pairs;
+      b_ = bg / p.heads_kv;
+      g_ = bg - b_ * p.heads_kv;
+      hq0_ = g_ * p.group + pr * NQ;  // q head of query tile s = hq0 + s
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        qi_a[t] = qi_;
+        hq_a[t] = hq0_ + t;
+      }
+    }
+  }
+  const int b = b_, g = g_, qi = qi_, hq0 = hq0_;
   // 128-key steps: causal -> through the frontier step i; calibration -> the
   // off-frontier prefix only (calibration.py:110-113)
   const int nsteps = CALIB ? qi : (p.causal ? qi + 1 : p.num_steps);
+#pragma unroll
+  for (int t = 0; t < NQ; ++t)
+    ns_a[t] = qi_a[t] < 0 ? 0 : (CALIB ? qi_a[t] : (p.causal ? qi_a[t] + 1 : p.num_steps));
   const int gate_mode = p.gate_mode;
   const int window = p.gate_window;
   const bool causal = p.causal != 0;
@@ -408,7 +442,8 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       for (int s = 0; s < NQ; ++s)
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d_w(sQ + s * C::Q_TILE + c * 128 * 128, &tm_q, bar_q, c * 64, qi * 128, hq0 + s, b, kEvictFirst);
+          tma_load_4d_w(sQ + s * C::Q_TILE + c * 128 * 128, &tm_q, bar_q, c * 64, (qi_a[s] < 0 ? 0 : qi_a[s]) * 128,
+                        hq_a[s], b, kEvictFirst);
       for (int j = 0; j < nsteps; ++j) {
         const int st = j % KS;
         mbar_wait((k_empty + 8 * (st)), ((j / KS) & 1) ^ 1);
@@ -484,30 +519,31 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
                           kEvictLast);
           ++vcount;
         };
+        unsigned dn_a[NQ] = {};  // dynamic steps consumed per query tile
         for (int j = 0; j < nsteps; ++j) {
-          const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
-          if (sb >= 0) {
+          // query tile 0's keeps are fetched as soon as its decision is known
+          // (statically or by its vote); the tiles only tile 1 keeps follow its
+          // decision (same order in the MMA warp)
+          uint32_t prev = 0;
 #pragma unroll
-            for (int h = 0; h < GT; ++h)
-              if ((sb >> h) & 1) load_unit(j, h);
-          } else {
-            // query tile 0's keeps are fetched as soon as its vote is in; the
-            // tiles only tile 1 keeps follow its vote (same order in the MMA warp)
-            uint32_t prev = 0;
-            const int di = int(dn % DQ);
-            const uint32_t ph = (dn / DQ) & 1;
-#pragma unroll
-            for (int s = 0; s < NQ; ++s) {
-              mbar_wait((dec_full + 8 * (s * DQ + di)), ph);
-              const uint32_t w = lds_u32(dec_sm + (s * DQ + di) * 4);
+          for (int s = 0; s < NQ; ++s) {
+            if (j >= ns_a[s]) continue;
+            const int sbs = step_static_bits<GT>(gate_mode, window, j, qi_a[s]);
+            uint32_t w;
+            if (sbs >= 0) {
+              w = uint32_t(sbs);
+            } else {
+              const int di = int(dn_a[s] % DQ);
+              mbar_wait((dec_full + 8 * (s * DQ + di)), (dn_a[s] / DQ) & 1);
+              w = lds_u32(dec_sm + (s * DQ + di) * 4);
               __syncwarp();
               mbar_arrive_w((dec_empty + 8 * (s * DQ + di)));
-#pragma unroll
-              for (int h = 0; h < GT; ++h)
-                if (((w & ~prev) >> h) & 1u) load_unit(j, h);
-              prev |= w;
+              ++dn_a[s];
             }
-            ++dn;
+#pragma unroll
+            for (int h = 0; h < GT; ++h)
+              if (((w & ~prev) >> h) & 1u) load_unit(j, h);
+            prev |= w;
           }
         }
         }
@@ -543,12 +579,15 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         const uint32_t d_tmem = CALIB ? tmem + (2 * s + (j & 1)) * 128 : tmem + C::S_COL + s * 128;
         umma_qk_tile_w<D, 128>(d_tmem, dq0 + uint64_t((s * C::Q_TILE) >> 4),
                                dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
-        if (s == NQ - 1) umma_commit_w((k_empty + 8 * (st)));
+        // the K stage is released by the last query tile that reads it (tile 1 of a
+        // block pair has no QK at tile 0's frontier step)
+        if (s == ((NQ == 2 && j < ns_a[NQ - 1]) ? NQ - 1 : 0)) umma_commit_w((k_empty + 8 * (st)));
         umma_commit_w(CALIB && (j & 1) ? (o_full + 8 * (s)) : (s_full + 8 * (s)));
       };
 
 #pragma unroll
-      for (int s = 0; s < NQ; ++s) issue_qk(s, 0);
+      for (int s = 0; s < NQ; ++s)
+        if (ns_a[s] > 0) issue_qk(s, 0);
       if constexpr (CALIB) {
         // QK_s(j+2) goes into the buffer the softmax released for step j
         if (nsteps > 1)
@@ -574,12 +613,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         // second half was measured slower.)
         uint32_t p1_par = 0;  // bit s: phase parity of p_full[s][1]
         for (int j = 0; j < nsteps; ++j) {
-          const int sb = step_static_bits<GT>(gate_mode, window, j, qi);
           uint32_t prev = 0;
           unsigned nunits = 0;
           unsigned uidx[GT];
 #pragma unroll
           for (int s = 0; s < NQ; ++s) {
+            if (j >= ns_a[s]) continue;
+            const int sb = step_static_bits<GT>(gate_mode, window, j, qi_a[s]);
             mbar_wait((p_full + 8 * (2 * s)), j & 1);
             tc_fence_after();
             const uint32_t bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + s * 4);
@@ -594,7 +634,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
                           dv0 + uint64_t(((u % VS) * C::V_UNIT) >> 4), IDESC_PV, (o_started >> s) & 1u);
               o_started |= 1u << s;
             }
-            if (j + 1 < nsteps) issue_qk(s, j + 1);  // S_s is free once P half 0 is consumed
+            if (j + 1 < ns_a[s]) issue_qk(s, j + 1);  // S_s is free once P half 0 is consumed
             constexpr int x1 = GT == 2 ? 1 : 0;
             if ((bits >> x1) & 1u) {
               // released for kept second halves only: phase = this tile's count of them
@@ -609,7 +649,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
               o_started |= 1u << s;
             }
             umma_commit_w((pv_done + 8 * (s)));
-            if (j == nsteps - 1) umma_commit_w((o_full + 8 * (s)));
+            if (j == ns_a[s] - 1) umma_commit_w((o_full + 8 * (s)));
           }
           for (unsigned x = 0; x < nunits; ++x) umma_commit_w((v_empty + 8 * ((vbase + x) % VS)));
           vbase += nunits;
@@ -948,7 +988,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     const int s = warp >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;  // row inside the query tile == TMEM lane
-    const int hq = hq0 + s;
+    const int hq = hq_a[s];
+    const int qi_s = qi_a[s];      // this tile's query block
+    const int nst = ns_a[s];       // this tile's steps (a block pair's tile 1 has one fewer)
+    if (!CALIB && nst == 0) {      // a block pair's missing second block (odd block count)
+      named_bar_arrive(15, C::NUM_THREADS);
+      return;
+    }
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const uint32_t s_row = tmem + lane_off + C::S_COL + s * 128;
     const uint32_t o_row = tmem + lane_off + C::O_COL + s * D;
@@ -960,7 +1006,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 
     float T = 0.f;
     if (!CALIB && p.gate_mode == kGateThreshold) {
-      const int pos = qi < p.thr_positions - 1 ? qi : p.thr_positions - 1;
+      const int pos = qi_s < p.thr_positions - 1 ? qi_s : p.thr_positions - 1;
       T = p.thr[(long long)hq * p.thr_positions + pos];
     }
 
@@ -981,7 +1027,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     auto turn_pass = [&]() {
       if (kTurn) named_bar_arrive(5 + (s ^ 1), 256);
     };
-    for (int j = 0; j < nsteps; ++j) {
+    for (int j = 0; j < nst; ++j) {
       if (BSFA_TURN == 2) turn_wait(j);
       if constexpr (CALIB)
         mbar_wait((j & 1) ? (o_full + 8 * (s)) : (s_full + 8 * (s)), (j >> 1) & 1);
@@ -995,9 +1041,9 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_buf + c, &sv[c]);
       tmem_wait_ld();
 
-      const int sb = CALIB ? -1 : step_static_bits<GT>(gate_mode, window, j, qi);
+      const int sb = CALIB ? -1 : step_static_bits<GT>(gate_mode, window, j, qi_s);
       if (!CALIB) {
-        if (j == qi && causal) {  // frontier step: key offset c vs row r inside block i
+        if (j == qi_s && causal) {  // frontier step: key offset c vs row r inside block i
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c > r) sv[c] = __float_as_uint(-INFINITY);
@@ -1089,10 +1135,10 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           sts_u32(decm_sm + s * 4, bits);
           kept_tiles += __popc(bits);
           if (p.decisions) {
-            int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi) * p.gate_cols;
+            int8_t* drow = p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi_s) * p.gate_cols;
 #pragma unroll
             for (int x = 0; x < GT; ++x)
-              drow[j * GT + x] = j == qi ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+              drow[j * GT + x] = j == qi_s ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
           }
         }
         if (sb < 0) ++dn;
@@ -1286,7 +1332,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       tc_fence_after();
       const float inv_l = 1.f / l_sum;
       bool bad = !(l_sum > 0.f);
-      const int row = qi * 128 + r;
+      const int row = qi_s * 128 + r;
       const long long orow = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)row * p.o_sn;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
@@ -1297,7 +1343,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           float a0 = __uint_as_float(ov[e]) * inv_l, a1 = __uint_as_float(ov[e + 1]) * inv_l;
-          if (p.inject_fault && qi == 0 && r == 0 && s == 0 && c == 0 && e == 0) a0 += 1.0f;  // O[0][0] += 1
+          if (p.inject_fault && qi_s == 0 && r == 0 && hq == 0 && c == 0 && e == 0) a0 += 1.0f;  // O[0][0] += 1
           bad |= !isfinite(a0) || !isfinite(a1);
           pk[e / 2] = pack_bf16x2(a0, a1);
         }
@@ -1306,7 +1352,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
       p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
       if (bad && p.status) atomicOr(p.status, 1);
       if (r == 0 && p.counters) {
-        atomicAdd(&p.counters[0], (unsigned long long)nsteps * GT);
+        atomicAdd(&p.counters[0], (unsigned long long)nst * GT);
         atomicAdd(&p.counters[1], kept_tiles);
       }
     }
