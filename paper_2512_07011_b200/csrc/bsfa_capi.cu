@@ -335,7 +335,13 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   // two-tile pipeline still runs (main kernel, one thread per row, second-half P
   // in shared memory)
   const bool main_path = !((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64);
-  p.block_pair = (p.group % 2 == 1 && main_path && BSFA_TPR == 1 && BSFA_P_SMEM && !BSFA_SPLIT_ISSUE) ? 1 : 0;
+#ifndef BSFA_BLOCK_PAIR_ALL
+#define BSFA_BLOCK_PAIR_ALL 0
+#endif
+  p.block_pair = ((p.group % 2 == 1 || BSFA_BLOCK_PAIR_ALL) && main_path && BSFA_TPR == 1 && BSFA_P_SMEM &&
+                  !BSFA_SPLIT_ISSUE)
+                     ? 1
+                     : 0;
   const int nq = p.block_pair ? 2 : tiles_per_cta(p.group);
   const long long grid = p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
