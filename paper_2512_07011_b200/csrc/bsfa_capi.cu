@@ -403,8 +403,10 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.c_ties = a->tie_counts;
   p.c_maxima = a->block_maxima;
 
-  const int nq = tiles_per_cta(p.group);
-  const int grid = (a->heads_q / nq) * p.num_q_tiles;
+  // odd groups (MHA included): two query blocks of one head per CTA, as in the forward
+  p.block_pair = (p.group % 2 == 1 && !(BSFA_GATE_STEP && a->b_n == 64)) ? 1 : 0;
+  const int nq = p.block_pair ? 2 : tiles_per_cta(p.group);
+  const int grid = p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2) : (a->heads_q / nq) * p.num_q_tiles;
   return dispatch<true>(d, a->b_n, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
   // ---- work unit: (batch, kv head) major, heaviest query block first, the
   //      head pairs of the GQA group minor (every pair reads the same K/V)
   // per query tile s: query block qi_a[s], q head hq_a[s], steps ns_a[s]
-  const bool bpair = !CALIB && NQ == 2 && p.block_pair != 0;
+  const bool bpair = NQ == 2 && p.block_pair != 0;
   int qi_a[NQ], hq_a[NQ], ns_a[NQ];
   int b_, g_, qi_, hq0_;
   {
@@ -590,12 +590,13 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
         if (ns_a[s] > 0) issue_qk(s, 0);
       if constexpr (CALIB) {
         // QK_s(j+2) goes into the buffer the softmax released for step j
-        if (nsteps > 1)
 #pragma unroll
-          for (int s = 0; s < NQ; ++s) issue_qk(s, 1);
+        for (int s = 0; s < NQ; ++s)
+          if (ns_a[s] > 1) issue_qk(s, 1);
         for (int j = 0; j + 2 < nsteps; ++j) {
 #pragma unroll
           for (int s = 0; s < NQ; ++s) {
+            if (j + 2 >= ns_a[s]) continue;
             mbar_wait((p_full + 8 * (2 * s + (j & 1))), (j >> 1) & 1);
             issue_qk(s, j + 2);
           }
@@ -991,7 +992,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
     const int hq = hq_a[s];
     const int qi_s = qi_a[s];      // this tile's query block
     const int nst = ns_a[s];       // this tile's steps (a block pair's tile 1 has one fewer)
-    if (!CALIB && nst == 0) {      // a block pair's missing second block (odd block count)
+    if (qi_s < 0) {                // a block pair's missing second block (odd block count)
       named_bar_arrive(15, C::NUM_THREADS);
       return;
     }
@@ -1278,11 +1279,11 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
 
     if constexpr (CALIB) {
       // ---- order statistics of this row of gate-tile maxima (calibration.py:116-153)
-      const int A = nsteps * GT;
+      const int A = nst * GT;
       named_bar_sync(3 + s, 128);
       int* vals = cvals + s * C::MAXA;
       if (p.c_maxima) {
-        float* out = p.c_maxima + ((long long)hq * p.num_q_tiles + qi) * p.gate_cols;
+        float* out = p.c_maxima + ((long long)hq * p.num_q_tiles + qi_s) * p.gate_cols;
         for (int x = r; x < A; x += 128) out[x] = ordered_to_float(vals[x]);
       }
       int n2 = 1;
@@ -1315,7 +1316,7 @@ __global__ void __launch_bounds__(KCfg<D, GT, NQ, CALIB, TPR>::NUM_THREADS, 1)
           cut = ordered_to_float(vals[k]);
           tie = vals[k - 1] == vals[k];
         }
-        const long long idx = (((long long)r * p.c_num_layers + p.c_layer) * p.heads_q + hq) * p.c_positions + qi;
+        const long long idx = (((long long)r * p.c_num_layers + p.c_layer) * p.heads_q + hq) * p.c_positions + qi_s;
         if (isfinite(cut)) {
           p.c_sum[idx] += (double)cut;
           p.c_fin[idx] += 1;

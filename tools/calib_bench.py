@@ -19,8 +19,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--hkv", type=int, default=8, help="kv heads (32 q heads): 8 = Llama GQA, 32 = MHA")
     a = ap.parse_args()
-    n, hq, hkv, d = a.n, 32, 8, 128
+    n, hq, hkv, d = a.n, 32, a.hkv, 128
     tiles = bsfa.TileConfig(128, 64)
     q, k = model_dump_layer(0, 0, hq, hkv, n, d, device="cuda", with_v=False)
     cal = bsfa.Calibrator([82, 149, 231], tiles, 1, hq, n, d)
@@ -37,7 +38,7 @@ def main():
     m_q = n // 128
     tiles_scored = hq * sum(2 * i for i in range(m_q))  # off-frontier gate tiles j < 2i per query block
     flops = 2.0 * 128 * 64 * d * tiles_scored
-    print(json.dumps({"n": n, "ms_per_layer": ms, "qk_tflops": flops / (ms * 1e-3) / 1e12}))
+    print(json.dumps({"n": n, "heads_kv": hkv, "ms_per_layer": ms, "qk_tflops": flops / (ms * 1e-3) / 1e12}))
 
 
 if __name__ == "__main__":
