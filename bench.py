@@ -70,14 +70,36 @@ def parse_args():
 
 
 # ----------------------------------------------------------------------------- helpers
-def measured_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def measured_peaks(path=None):
+    """(burst, sustained, source) dense bf16 TFLOP/s from the driver's MEASURED_PEAKS.json.
+
+    The file's exact layout is not fixed here: every numeric leaf whose key path
+    mentions bf16 (or matmul / tensor) and TFLOP is collected; one mentioning
+    "sustain" is the sustained figure, the largest other one the burst figure.
+    Falls back to the B200_PROFILING.md figures when the file is absent.
+    """
+    path = path or os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
-            p = json.load(f)
-        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+            doc = json.load(f)
     except Exception:
         return 1590.0, 1400.0, "fallback"
+    burst, sustained = [], []
+
+    def walk(node, keypath):
+        if isinstance(node, dict):
+            for k, v in node.items():
+                walk(v, keypath + "/" + str(k).lower())
+        elif isinstance(node, (int, float)) and not isinstance(node, bool):
+            kp = keypath
+            if ("bf16" in kp or "matmul" in kp or "tensor" in kp) and ("tflop" in kp or "tf/s" in kp or "tfs" in kp):
+                (sustained if "sustain" in kp else burst).append(float(node))
+
+    walk(doc, "")
+    if not burst and not sustained:
+        return 1590.0, 1400.0, "fallback"
+    b = max(burst) if burst else max(sustained)
+    return b, (max(sustained) if sustained else b), "measured"
 
 
 def committed_traffic():

@@ -245,3 +245,16 @@ def test_struct_offsets_match_the_c_compiler(tmp_path):
         assert int(got[cname]) == ctypes.sizeof(cls), cname
         for f in cls._fields_:
             assert int(got[f"{cname}.{f[0]}"]) == getattr(cls, f[0]).offset, (cname, f[0])
+
+
+def test_bench_reads_measured_peaks_in_any_layout(tmp_path):
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    for doc in ({"bf16_tflops": 1616.9, "bf16_tflops_sustained": 1390.4},
+                {"bf16_dense_tflops": {"burst": 1616.9, "sustained_4s": 1390.4}, "hbm_gbps": 6549.8}):
+        f = tmp_path / "peaks.json"
+        f.write_text(json.dumps(doc))
+        assert bench.measured_peaks(str(f)) == (1616.9, 1390.4, "measured")
+    assert bench.measured_peaks(str(tmp_path / "absent.json"))[2] == "fallback"
