@@ -473,7 +473,10 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus, "peak_source": peak_src,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                "algorithmic_flops_per_launch": f_exec}
+                "algorithmic_flops_per_launch": f_exec,
+                # north_star's HBM evidence: the committed ncu DRAM bytes over this run's launch time
+                "hbm_gbps": ((traffic or {}).get("dram_bytes_per_launch") or 0) / (mean_launch_ms * 1e-3) / 1e9
+                if traffic else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
