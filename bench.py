@@ -21,8 +21,10 @@ Reported (one JSON line on rank 0):
               time vs the measured bf16 peak (MEASURED_PEAKS.json)
   cpu_baseline  the oracle port of the reference engine on one host core
   dense_*     the same kernel with the DenseGate (T = -inf), for speedup
-Multi-GPU (torchrun): weak scaling, rank r owns batch element r (its own
-full 32-head workload), no data-path collective.
+  interleaved BSFA and dense timed ABAB after the timed region (steady state)
+Multi-GPU (torchrun, BASELINE configs[3]): 128K, kv-head groups sharded over
+the ranks (strong scaling), an NCCL all-gather of O inside every step; the
+line adds the kernel-only time and the epilogue peer-store (NVLink) variant.
 """
 
 from __future__ import annotations
@@ -53,19 +55,20 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="l32k")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
+                    help="default: l32k (configs[1]) on one GPU, l128k (configs[3]) under torchrun")
     ap.add_argument("--density", type=float, default=0.5, help="target kept fraction (predicted)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=None,
                     help="kv-head groups the host path pipelines (default: BsfaPlan.run_host's)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
-                    help="multi-GPU: batch = weak scaling (rank r owns batch element r); heads = strong scaling "
-                         "over kv-head groups of one batch-1 problem (configs[3])")
-    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "peer"],
-                    help="with --shard heads: assemble the full O on every rank inside every timed step -- "
-                         "nccl: all-gather after the kernel; peer: epilogue stores into symmetric memory")
+    ap.add_argument("--shard", choices=["batch", "heads"], default=None,
+                    help="multi-GPU: heads (default) = configs[3], kv-head groups of one batch-1 problem per rank "
+                         "(strong scaling); batch = rank r owns its own full problem (weak scaling)")
+    ap.add_argument("--gather", choices=["nccl", "none"], default=None,
+                    help="with --shard heads: all-gather O on every rank inside every timed step (default nccl); "
+                         "the line also reports the kernel alone and the epilogue peer-store variant")
     return ap.parse_args()
 
 
@@ -150,7 +153,11 @@ class ClockSampler:
                 try:
                     sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
                     rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                    self.samples.append((sm, rs))
+                    try:
+                        pw = nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+                    except Exception:
+                        pw = None
+                    self.samples.append((sm, rs, pw))
                 except Exception as e:
                     self._err = str(e)
                     return
@@ -168,10 +175,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [self._err or "no samples"], "samples": 0}
-        sm = [x for x, _ in self.samples]
-        reasons = sorted({n for _, rs in self.samples for n, bit in self.REASONS.items() if rs & bit})
+        sm = [x for x, _, _ in self.samples]
+        pw = [p for _, _, p in self.samples if p is not None]
+        reasons = sorted({n for _, rs, _ in self.samples for n, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 2 ms period, timed region only"}
+                "reasons": reasons, "power_w_median": statistics.median(pw) if pw else None,
+                "samples": len(self.samples), "source": "NVML, 2 ms period, timed region only"}
 
 
 def dist_setup(n_gpus):
@@ -273,44 +282,49 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline_port(cfg, tiles, T_slice, seconds_budget=20.0):
-    """Oracle port of the reference engine (engine.py:117-193) on one host core.
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    Sample: head 0 of the workload, query blocks taken from the end of the
-    sequence (longest rows first) until ~`seconds_budget` of work; value is
-    executed TFLOP/s over the tiles processed.
-    """
+
+def reference_package():
+    """The unmodified reference package installed in baseline/_ref (pip --target), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "bsfa")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import bsfa as ref
+        from bsfa import engine, gates, thresholds, tiling, core  # noqa: F401
+        return ref
+    except Exception:
+        return None
+
+
+def _ref_head_worker(argv):
+    """One full head through the reference's own flash_forward (engine.py:117-193), one thread."""
     import numpy as np
-    import torch
     from threadpoolctl import threadpool_limits
+    seed, h, n, d, T = argv
+    sys.path.insert(0, REF_DIR)
+    from bsfa.core import HeadInput
+    from bsfa.engine import flash_forward
+    from bsfa.gates import GateContext, ThresholdGate
+    from bsfa.thresholds import ThresholdTensor
+    from bsfa.tiling import TileConfig
     from oracle import bsfa_oracle as orc
-    from paper_2512_07011_b200 import costs
-
-    q, k, v = make_inputs(cfg, 0, "cuda")
-    qh, kh, vh = (x[0, 0].float().cpu().numpy() for x in (q, k, v))
-    del q, k, v
-    thr = np.asarray(T_slice[0], dtype=np.float32)
-    gate = orc.threshold_gate(thr)
-    n, d = cfg["seq_len"], cfg["head_dim"]
-    m_q = n // tiles.b_m
-    done_blocks, reach, kept = 0, 0, 0
-    t0 = time.perf_counter()
+    q, k, v = (orc.round_bf16(x) for x in orc.gen_random(n, d, seed=seed, head=h))
+    tiles = TileConfig(128, 64)
+    tt = ThresholdTensor(values=np.full((1, 1, 1, n // 128), T, dtype=np.float32), k_levels=(1,), n_max=n,
+                         b_m=128, b_n=64)
     with threadpool_limits(limits=1):
-        i = m_q - 1
-        while i >= 0 and time.perf_counter() - t0 < seconds_budget:
-            _, _, dec = orc.flash_forward(qh, kh, vh, True, tiles.b_m, tiles.b_n, gate, q_blocks=range(i, i + 1))
-            reach += int(np.count_nonzero(dec[i]))
-            kept += int(np.count_nonzero(dec[i] >= 2))
-            done_blocks += 1
-            i -= 1
-    dt = time.perf_counter() - t0
-    fl = costs.executed_flops(reach, kept, tiles, d)
-    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "cpu": cpu_model(), "kind": "port",
-            "sample": f"head 0, last {done_blocks} of {m_q} query blocks ({reach} tiles) of the {n}-token "
-                      f"workload, threshold gate, numpy oracle port, 1 thread, {dt:.1f} s"}
+        t0 = time.perf_counter()
+        _, trace = flash_forward(HeadInput(q, k, v), tiles, ThresholdGate(tt), GateContext(k_level=1))
+        dt = time.perf_counter() - t0
+    dec = trace.decisions
+    return int(np.count_nonzero(dec)), int(np.count_nonzero(dec >= 2)), dt
 
 
-def _ref_worker(argv):
+def _port_worker(argv):
+    """Oracle port of engine.py:117-193 on a bounded set of query blocks, one thread."""
     import numpy as np
     from threadpoolctl import threadpool_limits
     from oracle import bsfa_oracle as orc
@@ -325,75 +339,151 @@ def _ref_worker(argv):
     return int(np.count_nonzero(sel)), int(np.count_nonzero(sel >= 2)), dt
 
 
-def run_reference(args, cfg):
-    """--impl reference: the reference algorithm (oracle port) on all host cores."""
+def _threshold_for(d):
+    # ~50% block skip for N(0,1) inputs (off-frontier block-max median 3.84 at d=128)
+    return 3.84 if d == 128 else 3.94
+
+
+def cpu_baseline(cfg, tiles):
+    """Reference CPU path on one host core, bounded sample (rank 0, N = 1).
+
+    32K and shorter: one full head through the UNMODIFIED reference package
+    (baseline/_ref) -- kind "reference".  Longer sequences, or no reference
+    install: the oracle port on the last query blocks of head 0 until ~20 s --
+    kind "port".  Value = executed TFLOP/s over the tiles processed.
+    """
+    from paper_2512_07011_b200 import costs
+    n, d = cfg["seq_len"], cfg["head_dim"]
+    T = _threshold_for(d)
+    if reference_package() is not None and n <= 32768:
+        reach, kept, dt = _ref_head_worker((0, 0, n, d, T))
+        fl = costs.executed_flops(reach, kept, tiles, d)
+        return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "cpu": cpu_model(), "kind": "reference",
+                "sample": f"head 0 of the {n}-token workload ({reach} tiles), reference bsfa.engine.flash_forward "
+                          f"from baseline/_ref, ThresholdGate T={T}, 1 thread, {dt:.1f} s"}
+    m_q = n // tiles.b_m
+    done, reach, kept, t_tot = 0, 0, 0, 0.0
+    i = m_q - 1
+    while i >= 0 and t_tot < 20.0:
+        r, kp, dt = _port_worker((0, 0, n, d, tiles.b_m, tiles.b_n, [T], range(i, i + 1)))
+        reach, kept, t_tot, done, i = reach + r, kept + kp, t_tot + dt, done + 1, i - 1
+    fl = costs.executed_flops(reach, kept, tiles, d)
+    return {"value": fl / t_tot / 1e12, "unit": "TFLOP/s", "cores": 1, "cpu": cpu_model(), "kind": "port",
+            "sample": f"head 0, last {done} of {m_q} query blocks ({reach} tiles) of the {n}-token workload, "
+                      f"numpy oracle port of engine.py, T={T}, 1 thread, {t_tot:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on all host cores (rank 0 only).
+
+    N = 1 (32K): every core runs one full head of the workload through the
+    unmodified reference package in baseline/_ref (a step = `cores` heads);
+    at most one warm-up step (a CPU has nothing to warm).  Longer sequences
+    (the 128K multi-GPU config; one reference head takes ~140 s) or no
+    reference install: the oracle port on the two longest query blocks of a
+    head per core.
+    """
     import multiprocessing as mp
-    import numpy as np
     from paper_2512_07011_b200 import costs
     from paper_2512_07011_b200.tiling import TileConfig
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    config = args.config or ("l128k" if world > 1 else "l32k")
+    cfg = dict(CONFIGS[config])
     tiles = TileConfig(128, 64)
     n, d = cfg["seq_len"], cfg["head_dim"]
     m_q = n // tiles.b_m
     cores = os.cpu_count() or 1
-    thr = [3.84] if d == 128 else [3.94]
-    # one step: every core runs one head over a bounded block of query rows near the end
-    per = max(1, min(m_q, 2))
-    jobs = [(0, h % cfg["heads_q"], n, d, tiles.b_m, tiles.b_n, thr, range(m_q - per, m_q)) for h in range(cores)]
+    T = _threshold_for(d)
+    use_ref = reference_package() is not None and n <= 32768
+    if use_ref:
+        jobs = [(0, h % cfg["heads_q"], n, d, T) for h in range(cores)]
+        fn, warm = _ref_head_worker, min(args.warmup, 1)
+        sample = (f"{cores} processes x 1 thread, each one full head of the {n}-token workload through the "
+                  f"unmodified reference bsfa.engine.flash_forward (baseline/_ref), ThresholdGate T={T}")
+    else:
+        per = max(1, min(m_q, 2))
+        jobs = [(0, h % cfg["heads_q"], n, d, tiles.b_m, tiles.b_n, [T], range(m_q - per, m_q))
+                for h in range(cores)]
+        fn, warm = _port_worker, args.warmup
+        sample = (f"{cores} processes x 1 thread, each the last {per} query blocks of one head of the "
+                  f"{n}-token workload (threshold gate T={T}), numpy oracle port of engine.py")
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(cores) as pool:
-        for step in range(args.warmup + args.steps):
+        for step in range(warm + args.steps):
             t0 = time.perf_counter()
-            res = pool.map(_ref_worker, jobs)
+            res = pool.map(fn, jobs)
             dt = time.perf_counter() - t0
-            if step >= args.warmup:
-                fl = sum(costs.executed_flops(r, kp, tiles, d) for r, kp, _ in res)
-                times.append((dt, fl))
+            if step >= warm:
+                times.append((dt, sum(costs.executed_flops(r, kp, tiles, d) for r, kp, _ in res)))
     tot_t = sum(t for t, _ in times)
-    tot_f = sum(f for _, f in times)
-    val = tot_f / tot_t / 1e12
-    sample = (f"{cores} processes x 1 thread, each the last {per} query blocks of one head of the "
-              f"{n}-token workload (threshold gate), numpy oracle port of engine.py")
+    val = sum(f for _, f in times) / tot_t / 1e12
     line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(times),
+            "steps": args.steps, "warmup": warm, "ms_per_step": 1e3 * tot_t / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": args.config, **cfg, "tiles": "128x64", "causal": True},
-            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "cpu": cpu_model(), "kind": "port",
-                             "sample": sample},
+            "data": "synthetic", "config": {"workload": config, **cfg, "tiles": "128x64", "causal": True},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "cpu": cpu_model(),
+                             "kind": "reference" if use_ref else "port", "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ----------------------------------------------------------------------------- main
+def _median(x):
+    return statistics.median(x) if x else None
+
+
+def interleaved(arms, rounds, launches, stream, dev_index):
+    """ABAB timing: per round, `launches` timed launches of each arm in turn (steady state).
+
+    Returns {arm: {"ms": median per-launch ms, "all": [...], "sm_mhz": median, "power_w": median}}.
+    """
+    out = {name: {"all": [], "mhz": [], "w": []} for name in arms}
+    for _ in range(rounds):
+        for name, fn in arms.items():
+            with ClockSampler(dev_index) as cs:
+                _, t = time_steps(fn, launches, 0, stream)
+            out[name]["all"].append(t / launches)
+            out[name]["mhz"] += [x for x, _, _ in cs.samples]
+            out[name]["w"] += [w for _, _, w in cs.samples if w]
+    return {name: {"ms": _median(v["all"]), "all": [round(x, 4) for x in v["all"]],
+                   "sm_mhz": _median(v["mhz"]), "power_w": _median(v["w"])} for name, v in out.items()}
+
+
 def main():
     args = parse_args()
-    cfg = dict(CONFIGS[args.config])
     if args.impl == "reference":
-        return run_reference(args, cfg)
+        return run_reference(args)
 
-    import numpy as np
     import torch
     import paper_2512_07011_b200 as bsfa
     from paper_2512_07011_b200 import costs
 
     rank, world, local = dist_setup(args.gpus)
+    multi = world > 1
+    config = args.config or ("l128k" if multi else "l32k")
+    shard = args.shard or ("heads" if multi else "batch")
+    gather = args.gather or ("nccl" if (multi and shard == "heads") else "none")
+    cfg = dict(CONFIGS[config])
     dev = torch.device("cuda", local)
     tiles = bsfa.TileConfig(128, 64)
     n, d, hq, hkv = cfg["seq_len"], cfg["head_dim"], cfg["heads_q"], cfg["heads_kv"]
     k_level = costs.k_for_density(n, tiles, args.density)
     thr = calibrated_thresholds(cfg, tiles, k_level, dev)
+    backend = None
+    if multi:
+        import torch.distributed as dist
+        backend = dist.get_backend()
 
     stream = torch.cuda.current_stream(dev)
     head_offset = 0
-    gather_buf = None
-    peer_buf = None
-    if args.shard == "heads" and world > 1:
-        # strong scaling: rank r owns kv heads [r*Hkv/W, (r+1)*Hkv/W) of one problem
+    if shard == "heads" and multi:
+        # configs[3]: rank r owns kv heads [r*Hkv/W, (r+1)*Hkv/W) of one B = 1 problem
         from paper_2512_07011_b200.distributed import shard_heads
         sh = shard_heads(hq, hkv, world, rank)
         qf, kf, vf = make_inputs(cfg, 0, dev)
@@ -402,24 +492,26 @@ def main():
         v = vf[:, sh.kv_lo:sh.kv_hi].contiguous()
         del qf, kf, vf
         hq, hkv, head_offset = sh.num_q, sh.num_kv, sh.q_lo
-        if args.gather == "nccl":
-            gather_buf = torch.empty((world * hq, n, d), dtype=torch.bfloat16, device=dev)
-        elif args.gather == "peer":
-            from paper_2512_07011_b200.distributed import PeerGatherBuffer
-            peer_buf = PeerGatherBuffer.symmetric(1, world * hq, n, d, rank=rank, world=world, device=dev)
     else:
         q, k, v = make_inputs(cfg, rank, dev)  # rank r = batch element r (weak scaling)
     plan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level, head_offset=head_offset,
-                         device=dev, out=peer_buf.out if peer_buf is not None else None,
-                         o_peers=peer_buf.peers if peer_buf is not None else ())
+                         device=dev)
+
+    gather_buf = torch.empty((world * hq, n, d), dtype=torch.bfloat16, device=dev) if gather == "nccl" else None
+
+    def all_gather(o):
+        import torch.distributed as dist
+        if backend == "nccl":
+            dist.all_gather_into_tensor(gather_buf, o.view(hq, n, d))
+        else:  # gloo (one-device code-path runs): staged through host memory
+            parts = [torch.empty((hq, n, d), dtype=torch.bfloat16) for _ in range(world)]
+            dist.all_gather(parts, o.view(hq, n, d).cpu())
+            gather_buf.copy_(torch.cat(parts))
 
     def step():
         o = plan.run(q, k, v)
         if gather_buf is not None:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gather_buf, o.view(hq, n, d))
-        if peer_buf is not None:
-            peer_buf.barrier()
+            all_gather(o)
 
     barrier(world)
     torch.cuda.synchronize()
@@ -432,20 +524,59 @@ def main():
     reach, kept, vload, vunits = int(cnt[0]), int(cnt[1]), int(cnt[2]), int(cnt[3])
     f_exec = costs.executed_flops(reach, kept, tiles, d)
     f_dense = costs.dense_flops(reach, tiles, d)
-    ms_rank = total_ms / args.steps
-    ms = max_over_ranks(ms_rank, world)
+    ms = max_over_ranks(total_ms / args.steps, world)
     job_flops = sum_over_ranks(float(f_exec), world)
     value = job_flops / (ms * 1e-3) / 1e12
     mean_launch_ms = sum(per_step) / len(per_step)
 
-    # dense reference point: same kernel, DenseGate
+    # multi-GPU: the same step without the exchange, and with the epilogue's NVLink peer stores
+    exchange = None
+    if multi and shard == "heads":
+        _, t_kernel = time_steps(lambda: plan.run(q, k, v), args.steps, 1, stream)
+        mean_launch_ms = t_kernel / args.steps
+        exchange = {"gather": gather, "kernel_only_ms": max_over_ranks(mean_launch_ms, world),
+                    "kernel_only_value": job_flops / (max_over_ranks(mean_launch_ms, world) * 1e-3) / 1e12,
+                    "gather_bytes_per_rank": (world - 1) * hq * n * d * 2 if gather != "none" else 0}
+        peer = None
+        try:
+            if backend != "nccl":
+                raise RuntimeError(f"peer stores need NVLink peers (backend {backend})")
+            from paper_2512_07011_b200.distributed import PeerGatherBuffer
+            peer = PeerGatherBuffer.symmetric(1, world * hq, n, d, rank=rank, world=world, device=dev)
+            pplan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, thresholds=thr, k_level=k_level,
+                                  head_offset=head_offset, device=dev, out=peer.out, o_peers=peer.peers)
+
+            def peer_step():
+                peer.barrier()
+                pplan.run(q, k, v)
+                peer.barrier()
+
+            barrier(world)
+            _, t_peer = time_steps(peer_step, args.steps, 1, stream)
+            pms = max_over_ranks(t_peer / args.steps, world)
+            exchange["peer_gather_ms"] = pms
+            exchange["peer_gather_value"] = job_flops / (pms * 1e-3) / 1e12
+            del pplan
+        except Exception as e:  # reported in the line, not fatal
+            exchange["peer_gather"] = f"unavailable: {str(e).splitlines()[0][:160]}"
+
+    # dense reference point: the same kernel path with the DenseGate, timed ABAB with BSFA at steady state
     dense = {}
     if not args.no_dense:
         dplan = bsfa.BsfaPlan(1, hq, hkv, n, d, tiles=tiles, device=dev)
-        dt, dtot = time_steps(lambda: dplan.run(q, k, v), max(3, args.steps // 2), 2, stream)
-        dms = max_over_ranks(dtot / max(3, args.steps // 2), world)
-        dense = {"dense_ms_per_step": dms, "speedup_vs_dense": dms / ms,
-                 "dense_tflops": sum_over_ranks(float(f_dense), world) / (dms * 1e-3) / 1e12}
+        for _ in range(2):
+            dplan.run(q, k, v)
+        barrier(world)
+        rounds = 4 if n <= 65536 else 2
+        ab = interleaved({"bsfa": lambda: plan.run(q, k, v), "dense": lambda: dplan.run(q, k, v)},
+                         rounds, 3, stream, local)
+        b_ms = max_over_ranks(ab["bsfa"]["ms"], world)
+        d_ms = max_over_ranks(ab["dense"]["ms"], world)
+        dense = {"dense_ms_per_step": d_ms, "dense_tflops": sum_over_ranks(float(f_dense), world) / (d_ms * 1e-3) / 1e12,
+                 "speedup_vs_dense": d_ms / b_ms,
+                 "interleaved": {"protocol": f"{rounds} rounds x (3 BSFA launches, 3 dense launches), medians, "
+                                             "after the timed region (steady state)",
+                                 "bsfa_ms": b_ms, "dense_ms": d_ms, "bsfa": ab["bsfa"], "dense": ab["dense"]}}
         del dplan
 
     # end to end through the public API from pinned host buffers
@@ -461,8 +592,9 @@ def main():
         def e2e_step():  # q-head groups pipelined: H2D(c+1) | kernel(c) | D2H(c-1)
             plan.run_host(qh, kh, vh, oh, chunks=args.e2e_chunks)
 
-        et, etot = time_steps(e2e_step, max(3, args.steps // 2), 2, stream)
-        ems = max_over_ranks(etot / max(3, args.steps // 2), world)
+        k_e2e = max(3, args.steps // 2)
+        _, etot = time_steps(e2e_step, k_e2e, 2, stream)
+        ems = max_over_ranks(etot / k_e2e, world)
         e2e = {"value": job_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "pipeline": "q-head groups: H2D(c+1) | kernel(c) | D2H(c-1); copy, two compute and copy-back streams"}
@@ -476,38 +608,38 @@ def main():
                 "algorithmic_flops_per_launch": f_exec,
                 # north_star's HBM evidence: the committed ncu DRAM bytes over this run's launch time
                 "hbm_gbps": ((traffic or {}).get("dram_bytes_per_launch") or 0) / (mean_launch_ms * 1e-3) / 1e9
-                if traffic else None}
+                if traffic else None,
+                "traffic_note": (traffic or {}).get("note")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline_port(cfg, tiles, thr.layer_slice(k_level, 0))
+            cpu = cpu_baseline(cfg, tiles)
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 
     if rank == 0:
+        heads_mode = shard == "heads" and multi
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
+            "scaling": "strong" if heads_mode else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": args.config, "batch_per_gpu": 1,
-                       "global_batch": 1 if (args.shard == "heads" and world > 1) else world, **cfg,
+            "config": {"workload": config, "batch_per_gpu": 1, "global_batch": 1 if heads_mode else world, **cfg,
                        "tiles": "128x64", "causal": True, "k_level": k_level,
                        "predicted_density": costs.predicted_density(n, tiles, k_level),
                        "parallelism": (f"kv-head-group sharding x{world}" + (
-                           ", NCCL all-gather of O per step" if gather_buf is not None else
-                           ", O stored into every rank's symmetric buffer by the epilogue (NVLink)"
-                           if peer_buf is not None else ", no collective"))
-                       if (args.shard == "heads" and world > 1) else f"batch sharding x{world}, no collective",
-                       "l2": "inputs (Q/K/V 384 MiB at 32K) exceed the 126 MB L2; no explicit flush",
+                           f", {backend} all-gather of O inside every step" if gather_buf is not None else
+                           ", no collective")) if heads_mode else f"batch sharding x{world}, no collective",
+                       "l2": f"inputs (Q/K/V {(cfg['heads_q'] + 2 * cfg['heads_kv']) * n * d * 2 >> 20} MiB) "
+                             "exceed the 126 MB L2; no explicit flush",
                        "thresholds": "calibrated on a separate synthetic sample (seed 1000)"},
             "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / vunits,
-            "v_tile_fetches": {"loaded": vload, "loadable": vunits, "note": "one fetch per (CTA, gate tile) serves both q heads of the CTA"},
-            "effective_dense_tflops": sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12 if world == 1
-            else None,
-            **dense, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": args.steps, "per_step_ms": [round(x, 4) for x in per_step],
+            "v_tile_fetches": {"loaded": vload, "loadable": vunits,
+                               "note": "one fetch per (CTA, gate tile) serves both query tiles of the CTA"},
+            "effective_dense_tflops": sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12,
+            **dense, "exchange": exchange, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks, "gpu_launches": args.steps, "per_step_ms": [round(x, 4) for x in per_step],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

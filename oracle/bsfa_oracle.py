@@ -203,7 +203,7 @@ def flash_forward(q, k, v, causal, b_m, b_n, gate, record=None, q_blocks=None):
     return out[:valid], lse[:valid], dec
 
 
-def flash_forward_fast(q, k, v, causal, b_m, b_n, keep_fn, record=None):
+def flash_forward_fast(q, k, v, causal, b_m, b_n, keep_fn, record=None, q_blocks=None):
     """Same algorithm as :func:`flash_forward`, vectorised over query blocks.
 
     Processes key block j for every query block that reaches it in one
@@ -211,6 +211,8 @@ def flash_forward_fast(q, k, v, causal, b_m, b_n, keep_fn, record=None):
     arithmetic is the reference's (same tile scores, same update order);
     only BLAS blocking differs.  ``keep_fn(i_idx, j, smax) -> bool array``
     decides the gated tiles; ``record`` (dict) receives smax arrays per j.
+    ``q_blocks`` restricts the run to those query blocks (rows of the other
+    blocks come back NaN), e.g. the longest rows of a 128K head.
     """
     q = np.ascontiguousarray(q, dtype=np.float32)
     k = np.ascontiguousarray(k, dtype=np.float32)
@@ -231,8 +233,12 @@ def flash_forward_fast(q, k, v, causal, b_m, b_n, keep_fn, record=None):
     last = fr_hi - 1 if causal else np.full(m_q, m_kv - 1)
     q3 = q.reshape(m_q, b_m, d)
     rows = np.arange(n).reshape(m_q, b_m)
+    active = np.ones(m_q, dtype=bool)
+    if q_blocks is not None:
+        active[:] = False
+        active[list(q_blocks)] = True
     for j in range(m_kv):
-        idx = np.nonzero(last >= j)[0]
+        idx = np.nonzero((last >= j) & active)[0]
         if idx.size == 0:
             continue
         kj = k[j * b_n:(j + 1) * b_n]
@@ -269,11 +275,38 @@ def flash_forward_fast(q, k, v, causal, b_m, b_n, keep_fn, record=None):
         acc[ki] = acc[ki] * alpha[:, :, None] + pv
         l[ki] = l[ki] * alpha + p.sum(axis=2)
         m[ki] = m_new
-    if not np.isfinite(acc).all() or not (l > 0).all():
+    if not np.isfinite(acc[active]).all() or not (l[active] > 0).all():
         raise ArithmeticError("non-finite accumulator")
-    out = (acc / l[:, :, None]).reshape(n, d)
-    lse = (m + np.log(l)).reshape(n)
-    return out[:valid], lse[:valid], dec
+    with np.errstate(divide="ignore", invalid="ignore"):
+        out = (acc / l[:, :, None])
+        lse = m + np.log(l)
+    out[~active] = np.nan
+    lse[~active] = np.nan
+    return out.reshape(n, d)[:valid], lse.reshape(n)[:valid], dec
+
+
+# engine.py:157-171: s_max of every gated (off-frontier, causal) tile, without the softmax
+def tile_maxima_grid(q, k, b_m, b_n):
+    """(m_q, m_kv) grid of max(q_i k_j^T * scale) over each off-frontier causal tile; NaN elsewhere.
+
+    The statistic ThresholdGate compares (gates.py:77-78) for every gated tile of
+    a causal head, one sgemm per query block: the mask-parity checker for
+    sequences whose full forward oracle is too slow (128K tokens).
+    """
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k, dtype=np.float32)
+    n = padded_len(q.shape[0], b_m, b_n)
+    q, k = pad_rows(q, n), pad_rows(k, n)
+    scale = scale_for(q.shape[1])
+    m_q, m_kv = n // b_m, n // b_n
+    grid = np.full((m_q, m_kv), np.nan, dtype=np.float32)
+    for i in range(m_q):
+        a = off_frontier(i, b_m, b_n)
+        if a == 0:
+            continue
+        s = (q[i * b_m:(i + 1) * b_m] @ k[:a * b_n].T) * scale
+        grid[i, :a] = s.reshape(b_m, a, b_n).max(axis=(0, 2))
+    return grid
 
 
 # ----------------------------------------------------------------- thresholds

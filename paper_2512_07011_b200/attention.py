@@ -18,8 +18,8 @@ Semantics kept from the reference engine:
   - scale = float32(1/sqrt(d)) (engine.py:144); LSE = m + ln(l) in scaled
     natural-log units (engine.py:182);
   - a row with a non-finite accumulator or l <= 0 raises NumericError
-    (engine.py:178-179) when ``check_numerics`` is on (always on in the
-    drop-in, which synchronises anyway).
+    (engine.py:178-179) when ``check_numerics`` is on (the default, as in
+    the reference; always on in the drop-in, which synchronises anyway).
 Numerics differ by design: inputs are rounded to bf16, P is bf16 on the
 tensor cores, O is emitted in bf16 (tolerance documented in DESIGN.md).
 """
@@ -27,6 +27,8 @@ tensor cores, O is emitted in bf16 (tolerance documented in DESIGN.md).
 from __future__ import annotations
 
 import ctypes
+import weakref
+import zlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -104,11 +106,35 @@ def _as_kernel_operand(x: torch.Tensor, n_pad: int, d_pad: int) -> torch.Tensor:
     return x
 
 
+_THR_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _device_thresholds(thresholds: ThresholdTensor, k_level, layer: int, head_offset: int, hq: int,
+                       device) -> torch.Tensor:
+    """fp32 [Hq, P] threshold rows on ``device``, uploaded once per (tensor, level, layer, heads, device).
+
+    The cache is keyed on the ThresholdTensor object and re-validated by a
+    CRC of the slice, so repeated calls (every layer of every forward) do not
+    pay a synchronous host-to-device copy, and an in-place edit of ``values``
+    is still picked up.
+    """
+    sl = np.ascontiguousarray(thresholds.layer_slice(k_level, layer)[head_offset:head_offset + hq])
+    crc = zlib.crc32(sl.view(np.uint8))
+    per = _THR_CACHE.setdefault(thresholds, {})
+    key = (k_level, layer, head_offset, hq, str(device))
+    hit = per.get(key)
+    if hit is not None and hit[0] == crc:
+        return hit[1]
+    t = torch.from_numpy(sl).to(device)
+    per[key] = (crc, t)
+    return t
+
+
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = True,
               gate=None, thresholds: ThresholdTensor | None = None, layer: int = 0,
               k_level: int | None = None, head_offset: int = 0,
               tiles: TileConfig = TileConfig(), return_trace: bool = False,
-              inject_fault: bool = False, check_numerics: bool = False,
+              inject_fault: bool = False, check_numerics: bool = True,
               scale: float | None = None, out: torch.Tensor | None = None,
               o_peers=()) -> AttentionResult:
     """Block-sparse (or dense) causal/non-causal GQA attention forward.
@@ -118,6 +144,12 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     ``values[level, layer, head_offset + h, min(i, P-1)]``; otherwise ``gate``
     may be a DenseGate / FrontierOnlyGate / ThresholdGate object; with
     neither the run is dense.
+
+    ``check_numerics`` (default on, like the reference engine.py:178-179)
+    reads the kernel's status word after the launch -- one device sync -- and
+    raises :class:`NumericError` if any row had a non-finite accumulator or a
+    zero normaliser.  Pass ``False`` in stream-ordered serving loops (or use
+    :class:`BsfaPlan`) and inspect ``result.status`` when convenient.
 
     ``out`` (bf16 [B, Hq, n_pad, d_pad], unit head_dim stride, 16-byte aligned
     rows) receives O instead of a fresh tensor; ``o_peers`` are device
@@ -138,8 +170,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
         if head_offset + hq > thresholds.num_heads:
             raise ConfigurationError(
                 f"heads [{head_offset}, {head_offset + hq}) outside calibrated {thresholds.num_heads}")
-        sl = thresholds.layer_slice(k_level, layer)[head_offset:head_offset + hq]
-        thr_dev = torch.from_numpy(np.ascontiguousarray(sl)).to(q.device, non_blocking=False)
+        thr_dev = _device_thresholds(thresholds, k_level, layer, head_offset, hq, q.device)
         mode = _lib.GATE_THRESHOLD
     elif gate is not None:
         mode = kernel_gate_mode(gate)
@@ -273,11 +304,18 @@ class BsfaPlan:
     def __init__(self, batch: int, heads_q: int, heads_kv: int, seq_len: int, head_dim: int, *,
                  causal: bool = True, tiles: TileConfig = TileConfig(), thresholds: ThresholdTensor | None = None,
                  layer: int = 0, k_level: int | None = None, head_offset: int = 0, gate=None,
-                 return_trace: bool = False, device=None, out: torch.Tensor | None = None, o_peers=()):
-        """``out`` / ``o_peers``: as in :func:`attention` (caller-owned O, extra peer copies)."""
+                 return_trace: bool = False, device=None, out: torch.Tensor | None = None, o_peers=(),
+                 scale: float | None = None):
+        """``out`` / ``o_peers``: as in :func:`attention` (caller-owned O, extra peer copies).
+
+        ``scale`` defaults to float32(1/sqrt(head_dim)) (engine.py:144).  Heads
+        narrower than 64/128 that the caller zero-pads to a plan width must pass
+        the ORIGINAL head's scale (``reference_scale(d)``), or the softmax and
+        the threshold comparisons use the padded width's.
+        """
         require_kernel_tiles(tiles)
         if head_dim not in (64, 128):
-            raise InvalidInputError("plans take head_dim 64 or 128 (pad smaller heads)")
+            raise InvalidInputError("plans take head_dim 64 or 128 (pad smaller heads and pass their scale)")
         if heads_q % heads_kv:
             raise InvalidInputError(f"query heads {heads_q} must be a multiple of kv heads {heads_kv}")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -334,7 +372,7 @@ class BsfaPlan:
         a.seq_len, a.valid_len, a.head_dim = self.n_pad, seq_len, head_dim
         a.b_m, a.b_n = tiles.b_m, tiles.b_n
         a.causal = 1 if causal else 0
-        a.scale = reference_scale(head_dim)
+        a.scale = reference_scale(head_dim) if scale is None else float(np.float32(scale))
         a.inject_fault = 0
         a.gate_window, a.gate_lambda = gate_params(gate) if self.thr is None else (0, 0.0)
         a.num_o_peers = len(o_peers)
@@ -353,10 +391,11 @@ class BsfaPlan:
         a.q_stride_b, a.q_stride_h, a.q_stride_n = q.stride(0), q.stride(1), q.stride(2)
         a.k_stride_b, a.k_stride_h, a.k_stride_n = k.stride(0), k.stride(1), k.stride(2)
         a.v_stride_b, a.v_stride_h, a.v_stride_n = v.stride(0), v.stride(1), v.stride(2)
-        if reset_counters:
-            self.counters.zero_()
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(self.lib.bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
+        with torch.cuda.device(self.device):
+            if reset_counters:
+                self.counters.zero_()
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(self.lib.bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
         return self.o
 
     # ------------------------------------------------------------------ host-resident inputs
@@ -396,6 +435,11 @@ class BsfaPlan:
             chunks = max(c for c in range(1, min(16, hq // qmin) + 1) if valid(c))
         if chunks < 1 or not valid(chunks):
             raise ConfigurationError(f"{hq} q heads ({hkv} kv heads) cannot be cut into {chunks} chunks")
+        with torch.cuda.device(self.device):
+            return self._run_host(q_h, k_h, v_h, o_h, chunks, grp)
+
+    def _run_host(self, q_h, k_h, v_h, o_h, chunks, grp):
+        bsz, hq, n, d = self.shape_q
         dev = self.device
         if getattr(self, "_host_bufs", None) is None:
             self._host_bufs = (torch.empty(self.shape_q, dtype=torch.bfloat16, device=dev),

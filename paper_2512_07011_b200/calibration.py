@@ -158,7 +158,7 @@ class Calibrator:
         self.pos = torch.zeros(shape, dtype=torch.int32, device=dev)
         self.ties = torch.zeros(len(k_levels), dtype=torch.int64, device=dev)
         self.nonfinite = torch.zeros((), dtype=torch.bool, device=dev)
-        self.covered = np.zeros(self.num_positions, dtype=bool)
+        self.covered = np.zeros((num_layers, self.num_positions), dtype=bool)  # per (layer, position)
         self.sample_ids = []
         self._last = None
 
@@ -181,7 +181,9 @@ class Calibrator:
         if qd.shape[0] != self.num_heads:
             raise ConfigurationError(f"layer has {qd.shape[0]} q heads, calibrator expects {self.num_heads}")
         self.nonfinite |= ~(torch.isfinite(qd).all() & torch.isfinite(kd).all())
-        self.covered[: n_pad // self.tiles.b_m] = True
+        if not 0 <= layer < self.num_layers:
+            raise ConfigurationError(f"layer {layer} outside the calibrator's {self.num_layers} layers")
+        self.covered[layer, : n_pad // self.tiles.b_m] = True
         a = _lib.CalibArgs()
         a.q, a.k = qd.data_ptr(), kd.data_ptr()
         a.q_stride_h, a.q_stride_n = qd.stride(0), qd.stride(1)
@@ -210,7 +212,9 @@ class Calibrator:
         if bool(self.nonfinite.item()):
             raise InvalidInputError("non-finite activations in a calibration sample")
         if not self.covered.all():
-            raise ConfigurationError("some calibrated positions are covered by no sample")
+            missing = sorted({int(x) for x in np.nonzero(~self.covered.all(axis=1))[0]})
+            raise ConfigurationError(
+                f"some calibrated (layer, position) pairs are covered by no sample (layers {missing[:8]})")
         vals = torch.empty(self.sum.shape, dtype=torch.float32, device=self.device)
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device).cuda_stream

@@ -8,21 +8,12 @@
 #include <string>
 
 #include "../../include/bsfa_b200.h"
-#include "bsfa_kernel.cuh"
-// forward at b_n = 64, d = 128, GQA groups of 4k: the CTA-pair kernel (bsfa_kernel_pair.cuh)
-#ifndef BSFA_PAIR
-#define BSFA_PAIR 0
+#include "bsfa_fwd.cuh"     // K1: forward (also includes bsfa_kernel.cuh)
+// -DBSFA_FWD_V1=1 builds the round-1 forward (TMEM-aliased P half, bsfa_kernel.cuh)
+// instead of bsfa_fwd.cuh, for A/B timing only.
+#ifndef BSFA_FWD_V1
+#define BSFA_FWD_V1 0
 #endif
-// forward at b_n = 64: the Q-in-TMEM 64-key-step kernel (bsfa_kernel_qt.cuh)
-#ifndef BSFA_QT_FWD
-#define BSFA_QT_FWD 0
-#endif
-#ifndef BSFA_GATE_STEP
-#define BSFA_GATE_STEP 0
-#endif
-#include "bsfa_kernel_gs.cuh"
-#include "bsfa_kernel_qt.cuh"
-#include "bsfa_kernel_pair.cuh"
 
 static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
 
@@ -89,23 +80,29 @@ int make_map(CUtensorMap* m, const void* base, int d, int n, int h, int bsz, int
   return BSFA_OK;
 }
 
-// threads per softmax row of the forward kernel (1: 128 keys per thread, 2: 64)
-#ifndef BSFA_TPR
-#define BSFA_TPR 1
-#endif
+// The dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per (kernel instantiation, device).
+template <auto Kern>
+int ensure_smem_attr(int bytes) {
+  static bool done[64] = {};  // one array per kernel (template argument)
+  auto kern = Kern;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev >= 0 && dev < 64 && done[dev]) return BSFA_OK;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return BSFA_OK;
+}
 
+// calibration kernel K2 (and, with -DBSFA_FWD_V1=1, the round-1 forward)
 template <int D, int GT, int NQ, bool CALIB>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
            cudaStream_t st) {
-  constexpr int TPR = CALIB ? 1 : BSFA_TPR;
-  using C = KCfg<D, GT, NQ, CALIB, TPR>;
-  auto kern = bsfa_kernel<D, GT, NQ, CALIB, TPR>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_done = true;
-  }
+  using C = KCfg<D, GT, NQ, CALIB, 1>;
+  auto kern = bsfa_kernel<D, GT, NQ, CALIB, 1>;
+  if (int rc = ensure_smem_attr<bsfa_kernel<D, GT, NQ, CALIB, 1>>(C::SMEM_BYTES)) return rc;
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
@@ -113,103 +110,42 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
   return BSFA_OK;
 }
 
-template <int D, int NQ, bool CALIB>
-int launch_gs(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
-              cudaStream_t st) {
-  using C = GsCfg<D, NQ, CALIB>;
-  auto kern = bsfa_kernel_gs<D, NQ, CALIB>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_done = true;
-  }
+// forward K1 (bsfa_fwd.cuh)
+template <int D, int GT>
+int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+               cudaStream_t st) {
+  using C = FCfg<D, GT>;
+  auto kern = bsfa_fwd_kernel<D, GT>;
+  if (int rc = ensure_smem_attr<bsfa_fwd_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa forward launch");
   return BSFA_OK;
 }
 
-int launch_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p,
-                int units, cudaStream_t st) {
-  using C = PairCfg;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(bsfa_kernel_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_done = true;
-  }
-  if (units == 0) return BSFA_OK;
-  bsfa_kernel_pair<<<2 * units, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "bsfa pair kernel launch");
-  return BSFA_OK;
-}
-
-bool use_pair(int d, int b_n, int group) { return BSFA_PAIR && d == 128 && b_n == 64 && group % 4 == 0; }
-
-template <int D, int NQ>
-int launch_qt(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
-              cudaStream_t st) {
-  using C = QtCfg<D, NQ>;
-  auto kern = bsfa_kernel_qt<D, NQ>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_done = true;
-  }
-  if (grid == 0) return BSFA_OK;
-  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
-  return BSFA_OK;
-}
-
-// The 128-key-step kernel serves both gate widths (b_n = 64: two gate tiles
-// per step).  -DBSFA_GATE_STEP=1 builds the 64-key-step variant with a
-// double-buffered S ring instead (bsfa_kernel_gs.cuh; correct, tensor-bound,
-// but its 128x64x16 QK MMAs cost as much as 128x128x16 ones).
-// NQ = 2 query tiles (two q heads of one GQA group) per CTA when the group
-// size is even.
 template <bool CALIB>
 int dispatch(int d, int b_n, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& p, int grid, cudaStream_t st) {
-#define BSFA_GS(D_, NQ_) \
-  if (d == D_ && b_n == 64 && nq == NQ_) return launch_gs<D_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
+  if constexpr (!CALIB && !BSFA_FWD_V1) {
+#define BSFA_FWD(D_, BN_) \
+  if (d == D_ && b_n == BN_) return launch_fwd<D_, 128 / BN_>(tq, tk, tv, p, grid, st);
+    BSFA_FWD(64, 64)
+    BSFA_FWD(128, 64)
+    BSFA_FWD(64, 128)
+    BSFA_FWD(128, 128)
+#undef BSFA_FWD
+    return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
+  }
 #define BSFA_CASE(D_, BN_, NQ_) \
   if (d == D_ && b_n == BN_ && nq == NQ_) return launch<D_, 128 / BN_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
-#define BSFA_QT(D_, NQ_) \
-  if (d == D_ && b_n == 64 && nq == NQ_) return launch_qt<D_, NQ_>(tq, tk, tv, p, grid, st);
-  if constexpr (!CALIB && BSFA_QT_FWD) {
-    BSFA_QT(64, 1)
-    BSFA_QT(64, 2)
-    BSFA_QT(128, 1)
-    BSFA_QT(128, 2)
-  }
-#undef BSFA_QT
-#if BSFA_GATE_STEP
-  BSFA_GS(64, 1)
-  BSFA_GS(64, 2)
-  BSFA_GS(128, 1)
-  BSFA_GS(128, 2)
-#else
-  BSFA_CASE(64, 64, 1)
   BSFA_CASE(64, 64, 2)
-  BSFA_CASE(128, 64, 1)
   BSFA_CASE(128, 64, 2)
-#endif
-  BSFA_CASE(64, 128, 1)
   BSFA_CASE(64, 128, 2)
-  BSFA_CASE(128, 128, 1)
   BSFA_CASE(128, 128, 2)
 #undef BSFA_CASE
-#undef BSFA_GS
   return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
 }
-
-int tiles_per_cta(int group) { return group % 2 == 0 ? 2 : 1; }
 
 int check_tiles(int b_m, int b_n) {
   if (b_m != 128 || (b_n != 64 && b_n != 128))
@@ -263,8 +199,6 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (a->gate_mode < 0 || a->gate_mode > 4) return fail(BSFA_ERR_INVALID, "bad gate_mode %d", a->gate_mode);
   if (a->gate_mode == BSFA_GATE_WINDOW && a->gate_window < 0)
     return fail(BSFA_ERR_INVALID, "window must be >= 0, got %d", a->gate_window);
-  if (BSFA_GATE_STEP && a->gate_mode > BSFA_GATE_FRONTIER)
-    return fail(BSFA_ERR_INVALID, "gate mode %d not built into the gate-step variant", a->gate_mode);
   if (a->gate_mode == BSFA_GATE_THRESHOLD && (!a->thresholds || a->thr_positions < 1))
     return fail(BSFA_ERR_INVALID, "threshold gate needs a [heads_q][positions] threshold array");
   if (!a->q || !a->k || !a->v || !a->o || !a->lse) return fail(BSFA_ERR_INVALID, "null tensor pointer");
@@ -276,14 +210,11 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
-                       (((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64) ||
-                        use_pair(a->head_dim, a->b_n, a->heads_q / a->heads_kv))
-                           ? 64
-                           : 128,
-                       "k"))
+128, "k"))
     return rc;
   if (int rc =
-          make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b, a->b_n, "v"))
+          make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b,
+                   BSFA_FWD_V1 ? a->b_n : 64, "v"))
     return rc;
 
   KernelParams p;
@@ -326,23 +257,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   p.counters = a->counters;
   p.status = a->status;
 
-  if (use_pair(d, a->b_n, p.group)) {
-    const long long units = (long long)a->batch * (a->heads_q / 4) * p.num_q_tiles;
-    if (2 * units > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
-    return launch_pair(tq, tk, tv, p, (int)units, reinterpret_cast<cudaStream_t>(stream));
-  }
-  // odd GQA groups (MHA included): two query blocks of one q head per CTA, so the
-  // two-tile pipeline still runs (main kernel, one thread per row, second-half P
-  // in shared memory)
-  const bool main_path = !((BSFA_GATE_STEP || BSFA_QT_FWD) && a->b_n == 64);
-#ifndef BSFA_BLOCK_PAIR_ALL
-#define BSFA_BLOCK_PAIR_ALL 0
-#endif
-  p.block_pair = ((p.group % 2 == 1 || BSFA_BLOCK_PAIR_ALL) && main_path && BSFA_TPR == 1 && BSFA_P_SMEM &&
-                  !BSFA_SPLIT_ISSUE)
-                     ? 1
-                     : 0;
-  const int nq = p.block_pair ? 2 : tiles_per_cta(p.group);
+  // two query tiles per CTA: two q heads of one GQA group (even groups), or
+  // query blocks 2m+1 and 2m of one q head (odd groups, MHA included)
+  p.block_pair = p.group % 2 == 1 ? 1 : 0;
+  const int nq = 2;
   const long long grid = p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
@@ -371,7 +289,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   CUtensorMap tq, tk;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, 1, a->q_stride_n, a->q_stride_h, 0, 128, "q")) return rc;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, 1, a->k_stride_n, a->k_stride_h, 0,
-                       (BSFA_GATE_STEP && a->b_n == 64) ? 64 : 128, "k"))
+                       128, "k"))
     return rc;
 
   KernelParams p;
@@ -404,8 +322,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.c_maxima = a->block_maxima;
 
   // odd groups (MHA included): two query blocks of one head per CTA, as in the forward
-  p.block_pair = (p.group % 2 == 1 && !(BSFA_GATE_STEP && a->b_n == 64)) ? 1 : 0;
-  const int nq = p.block_pair ? 2 : tiles_per_cta(p.group);
+  p.block_pair = p.group % 2 == 1 ? 1 : 0;
+  const int nq = 2;
   const int grid = p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2) : (a->heads_q / nq) * p.num_q_tiles;
   return dispatch<true>(d, a->b_n, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }

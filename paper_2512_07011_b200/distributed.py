@@ -140,28 +140,41 @@ def sharded_attention(q, k, v, *, rank: int, world: int, thresholds=None, layer:
                       k_level=None, gather=False, group=None, compute=None, peer_buffer=None, **kw):
     """Run this rank's heads of a full [B, Hq, N, d] problem.
 
-    ``q``/``k``/``v`` may be the full tensors (sliced here) or already the
-    local shard (``q.shape[1] == Hq/W``).  ``gather``: False, True/"nccl"
-    (all-gather after the kernel) or "peer" (epilogue stores into
-    ``peer_buffer``, a :class:`PeerGatherBuffer`).  ``compute`` defaults to
-    :func:`attention`; tests substitute a CPU checker to exercise the
-    partition/gather logic without a GPU.
+    Without ``heads_q``/``heads_kv`` keywords, ``q``/``k``/``v`` are the FULL
+    tensors and this rank's heads are sliced out here.  To pass only the local
+    shard, give the full head counts: ``heads_q=Hq, heads_kv=Hkv`` -- then
+    ``q.shape[1]`` must be Hq (sliced here) or Hq/W (used as is); anything else
+    raises.  ``gather``: False, True/"nccl" (all-gather after the kernel) or
+    "peer" (epilogue stores into ``peer_buffer``, a :class:`PeerGatherBuffer`;
+    the returned gathered view aliases that buffer and is valid until the next
+    call that uses it).  ``compute`` defaults to :func:`attention`; tests
+    substitute a CPU checker to exercise the partition/gather logic without a GPU.
     """
     from .attention import attention
 
     compute = compute or attention
     full_q = kw.pop("heads_q", None)
     full_kv = kw.pop("heads_kv", None)
+    if (full_q is None) != (full_kv is None):
+        raise ConfigurationError("give both heads_q and heads_kv (the full head counts) or neither")
     hq = full_q if full_q is not None else q.shape[1]
     hkv = full_kv if full_kv is not None else k.shape[1]
     sh = shard_heads(hq, hkv, world, rank)
-    if q.shape[1] == hq and world > 1:
-        q = q[:, sh.q_lo:sh.q_hi]
-        k = k[:, sh.kv_lo:sh.kv_hi]
-        v = v[:, sh.kv_lo:sh.kv_hi]
+    if q.shape[1] == hq and k.shape[1] == hkv:
+        if world > 1:
+            q = q[:, sh.q_lo:sh.q_hi]
+            k = k[:, sh.kv_lo:sh.kv_hi]
+            v = v[:, sh.kv_lo:sh.kv_hi]
+    elif q.shape[1] != sh.num_q or k.shape[1] != sh.num_kv:
+        raise ConfigurationError(
+            f"q/k carry {q.shape[1]}/{k.shape[1]} heads: neither the full problem ({hq}/{hkv}) "
+            f"nor rank {rank}'s shard ({sh.num_q}/{sh.num_kv})")
     if gather == "peer":
         if peer_buffer is None:
             raise ConfigurationError('gather="peer" needs a PeerGatherBuffer')
+        # write-after-read: a faster rank's epilogue must not overwrite slots a
+        # peer is still reading from the previous call's gathered view
+        peer_buffer.barrier()
         res = compute(q, k, v, thresholds=thresholds, layer=layer, k_level=k_level, head_offset=sh.q_lo,
                       out=peer_buffer.out, o_peers=peer_buffer.peers, **kw)
         peer_buffer.barrier()

@@ -197,3 +197,25 @@ def test_two_rank_sharded_calibration_matches_single_process():
     results = sorted((result_q.get(timeout=10) for _ in range(2)), key=lambda x: x[0])
     for rank, values in results:
         np.testing.assert_array_equal(values, want)
+
+
+def test_sharded_attention_local_shard_needs_full_head_counts():
+    """A rank passing only its shard gets its own heads and threshold rows: with the full
+    counts given, the shard is used as is; an ambiguous head count raises instead of re-slicing."""
+    seen = {}
+
+    def capture(q, k, v, head_offset=0, **kw):
+        seen.update(hq=q.shape[1], hkv=k.shape[1], off=head_offset)
+        return _Res(q)
+
+    full_q, full_k = torch.zeros(1, 32, 8, 4), torch.zeros(1, 8, 8, 4)
+    sharded_attention(full_q[:, 16:], full_k[:, 4:], full_k[:, 4:], rank=1, world=2, compute=capture,
+                      heads_q=32, heads_kv=8)
+    assert seen == dict(hq=16, hkv=4, off=16)
+    sharded_attention(full_q, full_k, full_k, rank=1, world=2, compute=capture)
+    assert seen == dict(hq=16, hkv=4, off=16)
+    with pytest.raises(ConfigurationError):
+        sharded_attention(full_q[:, :8], full_k[:, :2], full_k[:, :2], rank=1, world=2, compute=capture,
+                          heads_q=32, heads_kv=8)
+    with pytest.raises(ConfigurationError):
+        sharded_attention(full_q, full_k, full_k, rank=0, world=2, compute=capture, heads_q=32)

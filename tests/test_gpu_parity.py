@@ -16,13 +16,18 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from conftest import GOLDEN, load_golden  # noqa: E402
+from conftest import GOLDEN, load_golden, record_metric  # noqa: E402
 from oracle import bsfa_oracle as orc  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
 EPS = 1e-3
 ATOL = 2e-2
+# Long rows average thousands of V rows, so |O| shrinks like 1/sqrt(kept keys) (~0.007 per element
+# at 32K) and an absolute bound cannot see a dropped or corrupted tile.  Per row the relative error
+# ||O_gpu - O_ref|| / ||O_ref|| is set by bf16 P and bf16 O (2^-9 relative rounding): ROW_RTOL.
+ROW_RTOL = 1e-2
+LSE_ATOL = 1e-3  # LSE = m*scale + ln(l): l is summed from the fp32 exponentials
 
 
 @pytest.fixture(scope="module")
@@ -45,6 +50,19 @@ def _mask_parity(dec_gpu, dec_ref, smax_ref, thr_of_block):
         if not (np.isfinite(s) and abs(s - thr_of_block(i)) <= EPS):
             bad.append((int(i), int(j), float(s), int(dec_gpu[i, j]), int(dec_ref[i, j])))
     return bad
+
+
+def _row_rel_err(o_gpu, o_ref):
+    """max over rows of ||o_gpu_r - o_ref_r|| / ||o_ref_r|| (rows of o_ref that are NaN ignored)."""
+    ok = np.isfinite(o_ref).all(axis=1)
+    num = np.linalg.norm(o_gpu[ok].astype(np.float64) - o_ref[ok], axis=1)
+    den = np.linalg.norm(o_ref[ok].astype(np.float64), axis=1)
+    return float((num / den).max())
+
+
+def _lse_err(lse_gpu, lse_ref):
+    ok = np.isfinite(lse_ref)
+    return float(np.abs(lse_gpu[ok].astype(np.float64) - lse_ref[ok]).max())
 
 
 def _smax_grid(record, shape):
@@ -402,10 +420,29 @@ def test_calibration_matches_reference_golden(bsfa):
     np.testing.assert_array_equal(np.isfinite(t.values), fin)
     np.testing.assert_array_equal(t.values[~fin], ref[~fin])
     assert np.abs(t.values[fin] - ref[fin]).max() <= 1e-4
+    # tie counts per level (calibration.py:150-153, summed over samples and positions)
+    assert [t.diagnostics.tie_counts[int(kk)] for kk in c["k_levels"]] == [int(x) for x in c["ties"]]
     prof = bsfa.collect_block_maxima(samples[0], bsfa.TileConfig(128, 64))  # sample id 1
     for p in range(8):
         vals = prof.maxima[(0, 1, p)]
         np.testing.assert_allclose(vals, c["maxima_sample1"][0, 1, p, :len(vals)], atol=1e-4)
+
+
+def test_calibration_tie_counts_match_oracle(bsfa):
+    """Repeated key tiles give bit-equal tile maxima: the tie test (calibration.py:150-153,
+    reference KAT ties [5,5,3]) must count the same ties on the GPU as in the oracle."""
+    rng = np.random.default_rng(33)
+    n, d = 1024, 64
+    q = orc.round_bf16(rng.standard_normal((1, 2, n, d)).astype(np.float32))
+    base = orc.round_bf16(rng.standard_normal((4, 64, d)).astype(np.float32))
+    k = np.concatenate([base[t % 4] for t in range(n // 64)])[None, None]  # 4 distinct tiles, repeated
+    k = np.repeat(k, 2, axis=1)
+    levels = [0, 1, 2, 3, 4, 5, 8]
+    t = bsfa.calibrate(bsfa.CalibrationDump(1, 2, d, [bsfa.CalibrationSample(0, q, k)]), levels,
+                       bsfa.TileConfig(128, 64))
+    _, _, ties = orc.calibrate([(0, q, k)], levels, 128, 64)
+    assert {kk: t.diagnostics.tie_counts[kk] for kk in levels} == {kk: int(ties[kk]) for kk in levels}
+    assert sum(ties.values()) > 0
 
 
 def test_topk_round_trip_on_gpu(bsfa):
@@ -478,16 +515,115 @@ def test_llama_shape_sampled_heads(bsfa, n, d, causal, b_n, T, heads):
         def keep_fn(i_idx, j, smax):
             return dec[i_idx, j] == orc.KEPT
 
-        o_ref, _, dec_ref = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n, keep_fn, record=rec)
+        o_ref, lse_ref, dec_ref = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n, keep_fn, record=rec)
         # mask parity: the GPU decision must agree with T on every tile away from the threshold
         for j, (i_idx, smax) in rec.items():
             far = np.abs(smax - T) > EPS
             want = np.where(smax > T, orc.KEPT, orc.SKIPPED)
             assert (dec[i_idx[far], j] == want[far]).all(), (h, j)
-        assert np.abs(res.o[0, h].float().cpu().numpy() - o_ref).max() <= ATOL
-        od_ref, _, _ = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n,
-                                              lambda i_idx, j, sm: np.ones(len(i_idx), bool))
-        assert np.abs(dense.o[0, h].float().cpu().numpy() - od_ref).max() <= ATOL
+        o_gpu = res.o[0, h].float().cpu().numpy()
+        tag = f"n{n}_d{d}_{'causal' if causal else 'full'}_bn{b_n}"
+        aerr = np.abs(o_gpu - o_ref).max()
+        rel = _row_rel_err(o_gpu, o_ref)
+        lerr = _lse_err(res.lse[0, h].cpu().numpy(), lse_ref)
+        record_metric(f"{tag}_bsfa_max_abs", aerr)
+        record_metric(f"{tag}_bsfa_row_rel", rel)
+        record_metric(f"{tag}_bsfa_lse_abs", lerr)
+        assert aerr <= ATOL
+        assert rel <= ROW_RTOL, (h, rel)
+        assert lerr <= LSE_ATOL, (h, lerr)
+        od_ref, lsed_ref, _ = orc.flash_forward_fast(qh, kh, vh, causal, 128, b_n,
+                                                     lambda i_idx, j, sm: np.ones(len(i_idx), bool))
+        od_gpu = dense.o[0, h].float().cpu().numpy()
+        drel = _row_rel_err(od_gpu, od_ref)
+        dlerr = _lse_err(dense.lse[0, h].cpu().numpy(), lsed_ref)
+        record_metric(f"{tag}_dense_max_abs", np.abs(od_gpu - od_ref).max())
+        record_metric(f"{tag}_dense_row_rel", drel)
+        record_metric(f"{tag}_dense_lse_abs", dlerr)
+        assert np.abs(od_gpu - od_ref).max() <= ATOL
+        assert drel <= ROW_RTOL, h
+        assert dlerr <= LSE_ATOL, h
+
+
+def test_negative_control_corrupted_v_tile(bsfa):
+    """The long-N output check must catch one wrong 64-key V tile (GPU input only) at 32K.
+
+    The decisions do not depend on V, so the oracle replays the same mask on the
+    clean V; rows that kept the corrupted tile must exceed ROW_RTOL while the
+    clean run stays inside it (engine.py:157-182: a kept tile enters every such row).
+    """
+    n, d = 32768, 128
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    q = torch.randn((1, 4, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, 1, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, 1, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, 4, n // 128), 3.84, dtype=np.float32), k_levels=(1,),
+                             n_max=n, b_m=128, b_n=64)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True)
+    dec = res.decisions[0, 0].cpu().numpy()
+    j_bad = 100  # an off-frontier gate tile kept by many query blocks
+    assert np.count_nonzero(dec[:, j_bad] == orc.KEPT) > 50
+    v_bad = v.clone()
+    v_bad[0, 0, j_bad * 64:(j_bad + 1) * 64] += 1.0
+    bad = bsfa.attention(q, k, v_bad, thresholds=t, k_level=1, return_trace=True)
+    assert torch.equal(bad.decisions, res.decisions)
+    qh, kh, vh = (x[0, 0].float().cpu().numpy() for x in (q, k, v))
+    o_ref, lse_ref, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+                                               lambda i_idx, j, sm: dec[i_idx, j] == orc.KEPT)
+    clean = _row_rel_err(res.o[0, 0].float().cpu().numpy(), o_ref)
+    corrupt = _row_rel_err(bad.o[0, 0].float().cpu().numpy(), o_ref)
+    record_metric("negative_control_clean_row_rel", clean)
+    record_metric("negative_control_corrupt_row_rel", corrupt)
+    record_metric("negative_control_corrupt_max_abs", np.abs(bad.o[0, 0].float().cpu().numpy() - o_ref).max())
+    assert clean <= ROW_RTOL, clean
+    assert corrupt > 5 * ROW_RTOL, corrupt
+    # the absolute north_star bound alone would not have noticed
+    assert np.abs(bad.o[0, 0].float().cpu().numpy() - o_ref).max() <= 0.5
+
+
+def test_llama_128k_sampled_heads(bsfa):
+    """configs[3] length (128K, Llama GQA-4 layout, two kv groups): full gated-tile mask parity on two
+    heads, output + LSE parity on the 8 longest query blocks, dense and ~50% skip.
+
+    Reference semantics: engine.py:151-182 (1,024 query blocks x 2,048 gate tiles), thresholds.py:87.
+    """
+    n, d, hq, hkv, T = 131072, 128, 8, 2, 3.84
+    gen = torch.Generator(device="cuda").manual_seed(128)
+    q = torch.randn((1, hq, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, hq, n // 128), T, dtype=np.float32), k_levels=(1,),
+                             n_max=n, b_m=128, b_n=64)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True)
+    dense = bsfa.attention(q, k, v)
+    cnt = res.counters.cpu().numpy()
+    assert 0.3 < 1 - cnt[1] / cnt[0] < 0.7
+    last = list(range(n // 128 - 8, n // 128))
+    for h in (0, 5):
+        g = h // (hq // hkv)
+        qh, kh, vh = (x[0, c].float().cpu().numpy() for x, c in ((q, h), (k, g), (v, g)))
+        dec = res.decisions[0, h].cpu().numpy()
+        grid = orc.tile_maxima_grid(qh, kh, 128, 64)
+        gated = np.isfinite(grid)
+        far = gated & (np.abs(grid - T) > EPS)
+        want = np.where(grid > T, orc.KEPT, orc.SKIPPED)
+        assert np.array_equal(dec[far], want[far]), h
+        assert np.all(dec[~gated & (dec != orc.UNREACHABLE)] == orc.FRONTIER)
+        o_ref, lse_ref, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+                                                   lambda i_idx, j, sm: dec[i_idx, j] == orc.KEPT, q_blocks=last)
+        rows = slice(last[0] * 128, n)
+        o_gpu = res.o[0, h].float().cpu().numpy()
+        record_metric("n131072_bsfa_last8_row_rel", _row_rel_err(o_gpu[rows], o_ref[rows]))
+        record_metric("n131072_bsfa_last8_lse_abs", _lse_err(res.lse[0, h].cpu().numpy()[rows], lse_ref[rows]))
+        record_metric("n131072_mask_band_tiles", np.count_nonzero(gated & ~far))
+        assert np.abs(o_gpu[rows] - o_ref[rows]).max() <= ATOL
+        assert _row_rel_err(o_gpu[rows], o_ref[rows]) <= ROW_RTOL, h
+        assert _lse_err(res.lse[0, h].cpu().numpy()[rows], lse_ref[rows]) <= LSE_ATOL, h
+        od_ref, lsed_ref, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+                                                     lambda i_idx, j, sm: np.ones(len(i_idx), bool), q_blocks=last)
+        od_gpu = dense.o[0, h].float().cpu().numpy()
+        assert _row_rel_err(od_gpu[rows], od_ref[rows]) <= ROW_RTOL, h
+        assert _lse_err(dense.lse[0, h].cpu().numpy()[rows], lsed_ref[rows]) <= LSE_ATOL, h
 
 
 @pytest.mark.parametrize("d", [64, 128])
@@ -655,3 +791,17 @@ def test_torch_ops_match_python_api(bsfa):
                         assert thr_h[li, b, h, p] == want
                     n_ties[li] += orc.is_tie(np.sort(bm_h[b, h, p, :len(desc)])[::-1], kk)
     assert ties.cpu().tolist() == n_ties
+
+
+def test_calibrator_requires_every_layer(bsfa):
+    """A streaming caller that never feeds a layer gets an error, not zero thresholds (reference
+    calibrate() always covers every layer, calibration.py:185-199)."""
+    rng = np.random.default_rng(5)
+    q = _dev(rng.standard_normal((2, 512, 64)).astype(np.float32))
+    k = _dev(rng.standard_normal((1, 512, 64)).astype(np.float32))
+    cal = bsfa.Calibrator([1], bsfa.TileConfig(128, 64), 2, 2, 512, 64)
+    cal.add_layer(0, 0, q, k)
+    with pytest.raises(bsfa.ConfigurationError):
+        cal.finish()
+    cal.add_layer(0, 1, q, k)
+    assert cal.finish().values.shape == (1, 2, 2, 4)

@@ -146,3 +146,24 @@ def test_round_bf16():
     assert r[2] == np.float32(1.0078125)
     assert np.isinf(r[5])
     np.testing.assert_array_equal(orc.round_bf16(r), r)
+
+
+def test_tile_maxima_grid_matches_block_maxima():
+    q, k, _ = orc.gen_random(1024, 64, seed=3)
+    grid = orc.tile_maxima_grid(q, k, 128, 64)
+    bm = orc.block_maxima(q, k, 128, 64)
+    for p, vals in enumerate(bm):
+        row = grid[p][np.isfinite(grid[p])]
+        np.testing.assert_array_equal(np.sort(row)[::-1], vals)
+
+
+def test_fast_oracle_query_block_subset():
+    q, k, v = orc.gen_random(1024, 64, seed=4)
+    full_o, full_l, full_d = orc.flash_forward_fast(q, k, v, True, 128, 64, lambda i, j, s: s > 3.9)
+    sub_o, sub_l, sub_d = orc.flash_forward_fast(q, k, v, True, 128, 64, lambda i, j, s: s > 3.9, q_blocks=[5, 7])
+    for i in (5, 7):
+        rows = slice(i * 128, (i + 1) * 128)
+        np.testing.assert_array_equal(sub_o[rows], full_o[rows])
+        np.testing.assert_array_equal(sub_l[rows], full_l[rows])
+        np.testing.assert_array_equal(sub_d[i], full_d[i])
+    assert np.isnan(sub_o[:128]).all()
