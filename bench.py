@@ -618,6 +618,7 @@ def main():
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 
+    eff_dense = sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12  # collective: every rank
     if rank == 0:
         heads_mode = shard == "heads" and multi
         line = {
@@ -637,7 +638,7 @@ def main():
             "skip_frac": 1.0 - kept / reach, "v_tiles_skipped_frac": 1.0 - vload / vunits,
             "v_tile_fetches": {"loaded": vload, "loadable": vunits,
                                "note": "one fetch per (CTA, gate tile) serves both query tiles of the CTA"},
-            "effective_dense_tflops": sum_over_ranks(float(f_dense), world) / (ms * 1e-3) / 1e12,
+            "effective_dense_tflops": eff_dense,
             **dense, "exchange": exchange, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clocks, "gpu_launches": args.steps, "per_step_ms": [round(x, 4) for x in per_step],
         }

@@ -8,12 +8,14 @@
 #include <string>
 
 #include "../../include/bsfa_b200.h"
-#include "bsfa_fwd.cuh"     // K1: forward (also includes bsfa_kernel.cuh)
-// -DBSFA_FWD_V1=1 builds the round-1 forward (TMEM-aliased P half, bsfa_kernel.cuh)
-// instead of bsfa_fwd.cuh, for A/B timing only.
-#ifndef BSFA_FWD_V1
-#define BSFA_FWD_V1 0
+#include "bsfa_fwd.cuh"     // K1 v2: per-tile S, all of P in shared memory (also includes bsfa_kernel.cuh)
+#include "bsfa_fwd3.cuh"    // K1 v3: shared S, P in TMEM
+// Forward implementation: 1 = round-1 kernel (TMEM-aliased P half, bsfa_kernel.cuh),
+// 2 = bsfa_fwd.cuh, 3 = bsfa_fwd3.cuh.
+#ifndef BSFA_FWD_IMPL
+#define BSFA_FWD_IMPL 3
 #endif
+#define BSFA_FWD_V1 (BSFA_FWD_IMPL == 1)
 
 static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
 
@@ -114,9 +116,15 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 template <int D, int GT>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
                cudaStream_t st) {
+#if BSFA_FWD_IMPL == 2
   using C = FCfg<D, GT>;
   auto kern = bsfa_fwd_kernel<D, GT>;
   if (int rc = ensure_smem_attr<bsfa_fwd_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
+#else
+  using C = FCfg3<D, GT>;
+  auto kern = bsfa_fwd3_kernel<D, GT>;
+  if (int rc = ensure_smem_attr<bsfa_fwd3_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
+#endif
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();

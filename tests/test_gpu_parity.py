@@ -26,8 +26,8 @@ ATOL = 2e-2
 # Long rows average thousands of V rows, so |O| shrinks like 1/sqrt(kept keys) (~0.007 per element
 # at 32K) and an absolute bound cannot see a dropped or corrupted tile.  Per row the relative error
 # ||O_gpu - O_ref|| / ||O_ref|| is set by bf16 P and bf16 O (2^-9 relative rounding): ROW_RTOL.
-ROW_RTOL = 1e-2
-LSE_ATOL = 1e-3  # LSE = m*scale + ln(l): l is summed from the fp32 exponentials
+ROW_RTOL = 1e-2  # observed <= 4.0e-3 on every checked head; a corrupted V tile gives ~1.15
+LSE_ATOL = 1e-4  # LSE = m*scale + ln(l), l summed from the fp32 exponentials: observed <= 4e-6 (profiles/)
 
 
 @pytest.fixture(scope="module")
