@@ -122,8 +122,23 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   if (int rc = ensure_smem_attr<bsfa_fwd_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
 #else
   using C = FCfg3<D, GT>;
-  auto kern = bsfa_fwd3_kernel<D, GT>;
-  if (int rc = ensure_smem_attr<bsfa_fwd3_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
+  // gate class and causality are template parameters of the v3 kernel
+  const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) = nullptr;
+  int rc = BSFA_OK;
+#define BSFA_GM(GM_, CA_)                                                                     \
+  if (gm == GM_ && (p.causal != 0) == CA_) {                                                  \
+    kern = bsfa_fwd3_kernel<D, GT, GM_, CA_>;                                                 \
+    rc = ensure_smem_attr<bsfa_fwd3_kernel<D, GT, GM_, CA_>>(C::SMEM_BYTES);                  \
+  }
+  BSFA_GM(0, true)
+  BSFA_GM(0, false)
+  BSFA_GM(1, true)
+  BSFA_GM(1, false)
+  BSFA_GM(2, true)
+  BSFA_GM(2, false)
+#undef BSFA_GM
+  if (rc) return rc;
 #endif
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);

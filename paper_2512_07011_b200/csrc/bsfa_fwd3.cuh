@@ -99,7 +99,11 @@ struct FCfg3 {
   static_assert(VS >= 2, "V ring must hold one step");
 };
 
-template <int D, int GT>
+// GM: gate class -- 0 ThresholdGate (voted), 1 statically known steps (DenseGate,
+// FrontierOnlyGate, SlidingWindowGate: no vote), 2 RunningMaxGate (voted).  GM and
+// CAUSAL are template parameters so the per-step softmax code carries no
+// runtime gate/causality branches (smaller loop body, fewer taken branches).
+template <int D, int GT, int GM, bool CAUSAL>
 __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     bsfa_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
@@ -167,12 +171,17 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
   }
   const int b = b_, g = g_;
-  const bool causal = p.causal != 0;
+  constexpr bool causal = CAUSAL;
 #pragma unroll
   for (int t = 0; t < 2; ++t) ns_a[t] = qi_a[t] < 0 ? 0 : (causal ? qi_a[t] + 1 : p.num_steps);
   const int nsteps = ns_a[0];  // tile 0 is never the shorter one
   const int gate_mode = p.gate_mode;
   const int window = p.gate_window;
+  // statically known decision bits of step j for query block qi (-1: voted)
+  auto sbits = [&](int j, int qi) -> int {
+    if constexpr (GM == 1) return step_static_bits<GT>(gate_mode, window, j, qi);
+    return j == qi ? (1 << GT) - 1 : -1;  // frontier (tiling.py:50-60)
+  };
   // debug timeline (-DBSFA_TRACE=1 builds only): clock64 per (event, tile, step) of one CTA
   const bool tr_cta = BSFA_TRACE && p.trace && (int)blockIdx.x == p.trace_cta;
   auto trace = [&](int ev, int s, int j) {
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           if (j >= ns_a[s]) continue;
-          const int sbs = step_static_bits<GT>(gate_mode, window, j, qi_a[s]);
+          const int sbs = sbits(j, qi_a[s]);
           uint32_t w;
           if (sbs >= 0) {
             w = uint32_t(sbs);
@@ -349,7 +358,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       unsigned uidx[2] = {0u, 0u};
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
       auto issue_pv = [&](int s, int j) {
-        const int sb = step_static_bits<GT>(gate_mode, window, j, qi_a[s]);
+        const int sb = sbits(j, qi_a[s]);
         mbar_wait(p_full + 16 * s + 8 * (j & 1), (j >> 1) & 1);
         tc_fence_after();
         if (lane == 0) trace(6, s, j);
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     const int valid_len = p.valid_len;
 
     float T = 0.f;
-    if (gate_mode == kGateThreshold) {
+    if constexpr (GM == 0) {
       const int pos = qi_s < p.thr_positions - 1 ? qi_s : p.thr_positions - 1;
       T = p.thr[(long long)hq * p.thr_positions + pos];  // thresholds.py:87
     }
@@ -451,13 +460,13 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(s_free);  // the other tile's QK may overwrite S
       if (r == 0) trace(1, s, j);
 
-      const int sb = step_static_bits<GT>(gate_mode, window, j, qi_s);
-      if (j == qi_s && causal) {  // frontier step: key offset c vs row r inside block i
+      const int sb = sbits(j, qi_s);
+      if (CAUSAL && j == qi_s) {  // frontier step: key offset c vs row r inside block i
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c > r) sv[c] = __float_as_uint(-INFINITY);
       }
-      if (!causal && (j + 1) * 128 > valid_len) {
+      if (!CAUSAL && (j + 1) * 128 > valid_len) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (j * 128 + c >= valid_len) sv[c] = __float_as_uint(-INFINITY);
@@ -489,12 +498,17 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       } else {
         mx[0] = fmaxf(mh[0], mh[1]);
       }
+      if (BSFA_TRACE && r == 0) {
+        // keep the clock read after the maxima (a dependent no-op on them)
+        asm volatile("" ::"f"(mx[0]));
+        trace(8, s, j);
+      }
 
       // ---- gate decision, OR over the tile's 128 rows in the barrier hardware
       uint32_t bits;
-      if (sb >= 0) {
+      if (GM == 1 || sb >= 0) {
         bits = uint32_t(sb);
-      } else if (gate_mode == kGateThreshold) {
+      } else if constexpr (GM == 0) {
         // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
         bits = 0;
 #pragma unroll
@@ -511,29 +525,33 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           if (k) mrun = fmaxf(mrun, mx[x]);
         }
       }
-      if (gate_mode == kGateRunMax) {
+      if constexpr (GM == 2) {
 #pragma unroll
         for (int x = 0; x < GT; ++x)
           if ((bits >> x) & 1u) m_true = fmaxf(m_true, mx[x]);
       }
-      if (r == 0) {
-        if (sb < 0) {
-          // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
-          // few steps at most -- it gates the PVs -- so this never spins in practice)
-          if (dn >= DQ)
-            while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
-            }
-          st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
-        }
-        sts_u32(decm_sm + (2 * s + (j & 1)) * 4, bits);
-        kept_tiles += __popc(bits);
-        if (drow) {
-#pragma unroll
-          for (int x = 0; x < GT; ++x)
-            drow[j * GT + x] = j == qi_s ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
-        }
+      if (BSFA_TRACE && r == 0) {
+        asm volatile("" ::"r"(bits));
+        trace(9, s, j);
       }
-      if (sb < 0) ++dn;
+      // bookkeeping spread over the tile's warps (every thread holds `bits`), so
+      // no single warp lags into the next vote
+      if (GM != 1 && r == 64 && sb < 0) {
+        // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
+        // few steps at most -- it gates the PVs -- so this never spins in practice)
+        if (dn >= DQ)
+          while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
+          }
+        st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
+      }
+      if (r == 32) sts_u32(decm_sm + (2 * s + (j & 1)) * 4, bits);
+      if (r == 96) kept_tiles += __popc(bits);
+      if (drow && r == 0) {
+#pragma unroll
+        for (int x = 0; x < GT; ++x)
+          drow[j * GT + x] = j == qi_s ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+      }
+      if (GM != 1 && sb < 0) ++dn;
       if (r == 0) trace(2, s, j);
       const uint32_t p_bar = p_full + 16 * s + 8 * (j & 1);
       if (bits == 0) {
@@ -657,7 +675,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
     p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
     if (bad && p.status) atomicOr(p.status, 1);
-    if (r == 0 && p.counters) {
+    if (r == 96 && p.counters) {
       atomicAdd(&p.counters[0], (unsigned long long)nst * GT);
       atomicAdd(&p.counters[1], kept_tiles);
     }

@@ -23,7 +23,7 @@ import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
 STEPS = 2048
-EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi"]
+EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi", "Max", "Bar"]
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
         plan = (bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, thresholds=thr, k_level=kl, device=dev)
                 if mode == "bsfa" else bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, device=dev))
         for cta in a.cta:
-            buf = torch.zeros((16, STEPS), dtype=torch.int64, device=dev)
+            buf = torch.zeros((20, STEPS), dtype=torch.int64, device=dev)
             plan.run(q, k, v)
             lib.bsfa_debug_trace(ctypes.c_void_p(buf.data_ptr()), cta)
             plan.run(q, k, v)
@@ -59,12 +59,15 @@ def main():
             out = {"mode": mode, "cta": cta, "steps": n,
                    "cycles_per_step": float((ev["Done"][1][n - 1] - ev["Done"][1][0]) / max(1, n - 1))}
             for s in range(2):
-                S, Ld, Vo, P0, Dn, QKi, PVs, PVi = (ev[x][s] for x in EV)
+                S, Ld, Vo, P0, Dn, QKi, PVs, PVi, Mx, Br = (ev[x][s] for x in EV)
                 o = s ^ 1
                 out[f"s{s}"] = {
                     "wait_S(Done_j-1->S_j)": float(np.median(S[1:] - Dn[:-1])),
                     "ld(S->Ld)": float(np.median(Ld - S)),
                     "vote(Ld->Vote)": float(np.median(Vo - Ld)),
+                    "  max(Ld->Max)": float(np.median(Mx - Ld)),
+                    "  bar(Max->Bar)": float(np.median(Br - Mx)),
+                    "  post(Bar->Vote)": float(np.median(Vo - Br)),
                     "half0(Vote->P0)": float(np.median(P0 - Vo)),
                     "rest(P0->Done)": float(np.median(Dn - P0)),
                     "softmax_busy(S->Done)": float(np.median(Dn - S)),
