@@ -1,5 +1,6 @@
-// BSFA forward (K1) for sm_100a, v3: one score buffer shared by the two query
-// tiles, P in tensor memory.
+// BSFA forward (K1) for sm_100a, v4: one score buffer shared by the two query
+// tiles, P in tensor memory, and each tile's softmax warps issue that tile's
+// own PV MMAs.
 //
 // One CTA owns two query tiles (128 rows each) that read the same K/V: two q
 // heads of one GQA group at query block i, or -- odd groups, MHA -- query
@@ -8,33 +9,34 @@
 // (tiling.py:19-69).
 //
 // TMEM (512 columns): O_0, O_1 (fp32, D columns each), ONE score buffer S
-// (fp32, 128 columns) and P_0, P_1 (bf16, 64 columns each).  The softmax
-// warps of a tile copy S into registers and release it at once (`s_free`),
-// so the tensor core computes the other tile's scores while this tile votes,
-// exponentiates and writes P_s; P never aliases S, so a tile's next QK never
-// waits for its own exponentials (the chain S -> softmax -> PV -> next QK of
-// a TMEM-aliased P is gone), and P stays in TMEM (tcgen05.st, TS-form PV:
-// no shared-memory stores, no P reads from shared memory).
+// (fp32, 128 columns) and P_0, P_1 (bf16 pairs, 64 columns each).  A tile's
+// softmax warps copy S into registers and release it at once (`s_free`), so
+// the tensor core computes the other tile's scores while this tile votes,
+// exponentiates and writes P_s.  P never aliases S, so no QK waits for an
+// exponential, and P stays in TMEM (tcgen05.st, TS-form PV).
 //
-// Tensor-pipe order (in-order), iteration j:
-//   QK_0(j+1)  PV_0(j)  QK_1(j+1)  PV_1(j)
-// QK_1(j+1) waits until tile 0 has read S(j+1); while it waits the pipe runs
-// PV_0(j), which hides the tcgen05.ld latency whenever tile 0 kept something.
-// Every wait of the issuer is on an event the next item depends on anyway
-// (tile 0 reads S(j+1) only after writing P_0(j)), so no tile blocks the other.
+// Issue: warp 9 issues only the QKs, strictly in the order QK_0(0) QK_1(0)
+// QK_0(1) QK_1(1) ..., each as soon as the previous owner of S has read it.
+// The PVs of tile s are issued by the tile's own warp 3 the moment its four
+// warps have written P_s(j) (named-barrier hand-off, no mbarrier round trip):
+// PV_s(j) therefore always enters the in-order tensor pipe before QK_{1-s}(j+1),
+// which can only be issued after tile s read S(j+1), and no issuing warp ever
+// serialises the two tiles' hand-offs (measured: the single issuer of v3 spent
+// ~1000 cycles per step in mbarrier round trips on the S chain).
 //
-// Shared memory: Q 2 x 128 rows x D, K ring of KC 64-column chunks (128 keys),
-// V ring of VS units of 64 keys x D (one unit per kept 64-key half).
+// V: each query tile has its own ring of VT units (64 keys x D), filled by its
+// own TMA producer warp (10 + s) from that tile's decisions only, so a tile
+// numbers its V units locally; a V gate tile is fetched iff the tile keeps it
+// (engine.py:172-174: skipped tiles read no V).
 //
 // Warp roles (384 threads):
-//   warps 0-3 / 4-7  softmax of query tile 0 / 1, thread r owns row r (TMEM lane r)
-//   warp 8           TMA: Q once, K chunks
-//   warp 9           tcgen05 issuer (one elected lane) + TMEM owner
-//   warp 10          TMA: V units, fetched only when some query tile kept them
-//   warp 11          idle (completes the warpgroup for setmaxnreg)
+//   warps 4s..4s+3   softmax of query tile s, thread r owns row r (TMEM lane r);
+//                    warp 4s+3 also issues PV_s and commits pv_done / v_empty / o_full
+//   warp 8           TMA: Q once, K in 64-column chunks
+//   warp 9           QK issuer (one elected lane) + TMEM owner
+//   warps 10, 11     TMA: V units of query tile 0 / 1
 // Per step and tile: QK = D/16 MMAs 128x128x16 (SS, K-major SW128); gate vote
 // rowmax*scale > T OR-reduced over the 128 rows by BAR.RED.OR (gates.py:77-78);
-// skipped gate tiles get no V TMA, no exponentials, no PV (engine.py:172-174);
 // kept ones run the lazily rescaled online softmax (engine.py:57-68) and
 // O_s += P_h V_h as 4 MMAs 128xDx16 (TS: P from TMEM, V MN-major SW128) per
 // 64-key half.
@@ -42,23 +44,17 @@
 
 #include "bsfa_kernel.cuh"
 
-#ifndef BSFA_FWD3_KC
-#define BSFA_FWD3_KC 0  // 0: default per head_dim
+#ifndef BSFA_FWD4_KC
+#define BSFA_FWD4_KC 0  // 0: default
 #endif
-#ifndef BSFA_FWD3_VS
-#define BSFA_FWD3_VS 0
-#endif
-// 1: QKs issued by warp 9, PVs by warp 11 (each waits only on its own inputs;
-// measured 20 % slower: PVs then queue behind QKs in the in-order tensor pipe);
-// 0: one issuer in the order QK_0(j+1) PV_0(j) QK_1(j+1) PV_1(j)
-#ifndef BSFA_FWD3_SPLIT
-#define BSFA_FWD3_SPLIT 0
+#ifndef BSFA_FWD4_VT
+#define BSFA_FWD4_VT 0
 #endif
 
 namespace bsfa {
 
 template <int D, int GT>
-struct FCfg3 {
+struct FCfg4 {
   static constexpr int BN = 128 / GT;           // gate tile width (reference b_n)
   static constexpr int NCH = D / 64;            // 64-column swizzle atoms along head_dim
   static constexpr int Q_TILE = 128 * D * 2;
@@ -66,49 +62,44 @@ struct FCfg3 {
   static constexpr int K_CHUNK = 128 * 128;     // 128 keys x 64 columns, bf16
   static constexpr int V_UNIT = 64 * D * 2;     // 64 keys of V
   static constexpr int V_ATOM = 64 * 128;       // 64 keys x 64 columns
-  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : 4;
-  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 128 ? 6 : 8);
-  static constexpr int DQ = 8;                  // decision ring depth (V producer)
+  static constexpr int KC = BSFA_FWD4_KC ? BSFA_FWD4_KC : 4;
+  static constexpr int VT = BSFA_FWD4_VT ? BSFA_FWD4_VT : (D == 128 ? 3 : 4);  // V units per query tile
+  static constexpr int DQ = 8;                  // decision ring depth (V producers)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
-  static constexpr int OFF_V = OFF_K + KC * K_CHUNK;
-  static constexpr int OFF_BAR = OFF_V + VS * V_UNIT;
-  // bar_q, k_full/empty[KC], v_full/empty[VS], s_full[2], s_free,
-  // p_full[2][2 parity], pv_done[2], o_full[2]
-  static constexpr int NUM_BARS = 1 + 2 * KC + 2 * VS + 2 + 2 + 4 + 2 + 2;
+  static constexpr int OFF_V = OFF_K + KC * K_CHUNK;    // [2 tiles][VT units]
+  static constexpr int OFF_BAR = OFF_V + 2 * VT * V_UNIT;
+  // bar_q, k_full/empty[KC], v_full/empty[2][VT], s_full[2], s_free, pv_done[2], o_full[2]
+  static constexpr int NUM_BARS = 1 + 2 * KC + 4 * VT + 2 + 1 + 2 + 2;
   static constexpr int OFF_DEC = (OFF_BAR + NUM_BARS * 8 + 15) / 16 * 16;  // u32 [2][DQ] tagged decisions
   static constexpr int OFF_DECC = OFF_DEC + 2 * DQ * 4;                    // u32 [2] decisions consumed
-  static constexpr int OFF_DECM = OFF_DECC + 2 * 4;                        // u32 [2][2 parity]
-  static constexpr int OFF_XCH = OFF_DECM + 4 * 4;                         // f32 [2][128] epilogue
-  static constexpr int OFF_TMEMPTR = OFF_XCH + 2 * 128 * 4;
+  static constexpr int OFF_TMEMPTR = OFF_DECC + 2 * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
-  static constexpr int O_COL = 0;          // O_s at s * D
-  static constexpr int S_COL = 2 * D;      // the shared score buffer
+  static constexpr int O_COL = 0;            // O_s at s * D
+  static constexpr int S_COL = 2 * D;        // the shared score buffer
   static constexpr int P_COL = S_COL + 128;  // P_s (bf16 pairs) at P_COL + s * 64
   static constexpr int TMEM_COLS = 512;
   static constexpr int NUM_THREADS = 12 * 32;
-  static constexpr int KPROD_WARP = 8, MMA_WARP = 9, VPROD_WARP = 10, PV_WARP = 11;
+  static constexpr int KPROD_WARP = 8, QK_WARP = 9, VPROD_WARP = 10;  // + tile
   static constexpr int REG_OTHER = 56;
-  static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8;                       // 168
+  static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8;                            // 168
   static constexpr int REG_SOFT = (NUM_THREADS * REG_LAUNCH - 128 * REG_OTHER) / 256 / 8 * 8;  // 224
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
   static_assert(D == 64 || D == 128, "head_dim 64 or 128");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(P_COL + 128 <= TMEM_COLS, "TMEM budget");
-  static_assert(KC >= NCH + 1 || KC >= 2, "K ring");
-  static_assert(VS >= 2, "V ring must hold one step");
+  static_assert(KC >= 2, "K ring");
+  static_assert(VT >= 2, "V ring must hold one step of a tile");
 };
 
 // GM: gate class -- 0 ThresholdGate (voted), 1 statically known steps (DenseGate,
-// FrontierOnlyGate, SlidingWindowGate: no vote), 2 RunningMaxGate (voted).  GM and
-// CAUSAL are template parameters so the per-step softmax code carries no
-// runtime gate/causality branches (smaller loop body, fewer taken branches).
+// FrontierOnlyGate, SlidingWindowGate: no vote), 2 RunningMaxGate (voted).
 template <int D, int GT, int GM, bool CAUSAL>
-__global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
-    bsfa_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = FCfg3<D, GT>;
-  constexpr int KC = C::KC, VS = C::VS, DQ = C::DQ, NCH = C::NCH;
+__global__ void __launch_bounds__(FCfg4<D, GT>::NUM_THREADS, 1)
+    bsfa_fwd4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
+  using C = FCfg4<D, GT>;
+  constexpr int KC = C::KC, VT = C::VT, DQ = C::DQ, NCH = C::NCH;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
@@ -120,19 +111,16 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   const uint32_t bar_q = sbase + C::OFF_BAR;
   const uint32_t k_full = bar_q + 8;
   const uint32_t k_empty = k_full + 8 * KC;
-  const uint32_t v_full = k_empty + 8 * KC;
-  const uint32_t v_empty = v_full + 8 * VS;
-  const uint32_t s_full = v_empty + 8 * VS;    // [2]  QK_s(j) landed in S
-  const uint32_t s_free = s_full + 16;         // the tile that owned S copied it to registers (4 warps)
-  const uint32_t p_full = s_free + 16;         // [2][2 parity]  P_s(j) written / step decided (4 warps)
-  const uint32_t pv_done = p_full + 32;        // [2]  PV_s(j) landed (every step): P_s is free again
-  const uint32_t o_full = pv_done + 16;        // [2]  last PV_s landed
-  // decision hand-off to the V producer: tagged words ((n + 1) << 4 | bits) in a
-  // DQ ring per tile, polled with volatile loads -- no mbarrier round trips on
-  // the softmax's critical path; dec_cons[s] = decisions the producer consumed
+  const uint32_t v_full = k_empty + 8 * KC;     // [2][VT]
+  const uint32_t v_empty = v_full + 16 * VT;    // [2][VT]
+  const uint32_t s_full = v_empty + 16 * VT;    // [2]  QK_s(j) landed in S
+  const uint32_t s_free = s_full + 16;          // the tile that owned S copied it to registers (4 warps)
+  const uint32_t pv_done = s_free + 8;          // [2]  the tile's last PV landed (one phase per PV step)
+  const uint32_t o_full = pv_done + 16;         // [2]  every PV_s landed
+  // decision hand-off to the V producers: tagged words ((n + 1) << 4 | bits) in a
+  // DQ ring per tile, polled with volatile loads; dec_cons[s] = decisions consumed
   const uint32_t dec_sm = sbase + C::OFF_DEC;
   const uint32_t dec_cons = sbase + C::OFF_DECC;
-  const uint32_t decm_sm = sbase + C::OFF_DECM;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -171,9 +159,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
   }
   const int b = b_, g = g_;
-  constexpr bool causal = CAUSAL;
 #pragma unroll
-  for (int t = 0; t < 2; ++t) ns_a[t] = qi_a[t] < 0 ? 0 : (causal ? qi_a[t] + 1 : p.num_steps);
+  for (int t = 0; t < 2; ++t) ns_a[t] = qi_a[t] < 0 ? 0 : (CAUSAL ? qi_a[t] + 1 : p.num_steps);
   const int nsteps = ns_a[0];  // tile 0 is never the shorter one
   const int gate_mode = p.gate_mode;
   const int window = p.gate_window;
@@ -195,24 +182,22 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       mbar_init(k_full + 8 * i, 1);
       mbar_init(k_empty + 8 * i, 1);
     }
-    for (int i = 0; i < VS; ++i) {
+    for (int i = 0; i < 2 * VT; ++i) {
       mbar_init(v_full + 8 * i, 1);
       mbar_init(v_empty + 8 * i, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(s_full + 8 * s, 1);
-      if (s == 0) mbar_init(s_free, 4);
-      mbar_init(p_full + 16 * s, 4);
-      mbar_init(p_full + 16 * s + 8, 4);
       mbar_init(pv_done + 8 * s, 1);
       mbar_init(o_full + 8 * s, 1);
     }
+    mbar_init(s_free, 4);
     fence_mbarrier_init();
   }
   if (warp == C::VPROD_WARP) {
-    for (int i = lane; i < 2 * DQ + 2; i += 32) sts_u32(dec_sm + 4 * i, 0u);  // dec ring + dec_cons
+    for (int i = lane; i < 2 * DQ + 2; i += 32) sts_u32(dec_sm + 4 * i, 0u);  // dec rings + dec_cons
   }
-  if (warp == C::MMA_WARP) {
+  if (warp == C::QK_WARP) {
     tmem_alloc(tmem_ptr, C::TMEM_COLS);
     tmem_relinquish();
   }
@@ -250,171 +235,107 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     __syncwarp();
     named_bar_arrive(15, C::NUM_THREADS);
     return;
-  } else if (warp == C::VPROD_WARP) {
+  } else if (warp >= C::VPROD_WARP) {
     setmaxnreg_dec<C::REG_OTHER>();
-    // ======================= TMA: V units kept by some query tile ======================
-    if (nsteps > 0) {
+    // ======================= TMA: V units this query tile kept ========================
+    const int s = warp - C::VPROD_WARP;
+    const int ns = s ? ns_a[1] : ns_a[0];
+    const int qs = s ? qi_a[1] : qi_a[0];
+    if (ns > 0) {
       if (lane == 0) tma_prefetch_desc(&tm_v);
-      unsigned vcount = 0;
-      unsigned dn_a[2] = {0u, 0u};
-      for (int j = 0; j < nsteps; ++j) {
-        // tile 0's keeps as soon as its decision is known, then the units only
-        // tile 1 keeps (the MMA warp numbers units in the same order)
-        uint32_t prev = 0;
+      unsigned vcount = 0, dn = 0;
+      const uint32_t vf = v_full + 8 * VT * s, ve = v_empty + 8 * VT * s;
+      const uint32_t vbuf = sV + s * VT * C::V_UNIT;
+      for (int j = 0; j < ns; ++j) {
+        const int sb = sbits(j, qs);
+        uint32_t w;
+        if (sb >= 0) {
+          w = uint32_t(sb);
+        } else {
+          const uint32_t slot_addr = dec_sm + (s * DQ + int(dn % DQ)) * 4;
+          uint32_t word = ld_volatile_u32(slot_addr);
+          while ((word >> 4) != dn + 1) word = ld_volatile_u32(slot_addr);
+          w = word & 0xFu;
+          ++dn;
+          __syncwarp();
+          if (lane == 0) st_volatile_u32(dec_cons + 4 * s, dn);
+        }
+        const uint32_t hb = GT == 2 ? w : (w ? 3u : 0u);  // 64-key halves kept
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (j >= ns_a[s]) continue;
-          const int sbs = sbits(j, qi_a[s]);
-          uint32_t w;
-          if (sbs >= 0) {
-            w = uint32_t(sbs);
-          } else {
-            const uint32_t slot_addr = dec_sm + (s * DQ + int(dn_a[s] % DQ)) * 4;
-            const uint32_t tag = dn_a[s] + 1;
-            uint32_t word = ld_volatile_u32(slot_addr);
-            while ((word >> 4) != tag) word = ld_volatile_u32(slot_addr);
-            w = word & 0xFu;
-            ++dn_a[s];
-            __syncwarp();
-            if (lane == 0) st_volatile_u32(dec_cons + 4 * s, dn_a[s]);
+        for (int hh = 0; hh < 2; ++hh) {
+          if ((hb >> hh) & 1u) {
+            const int slot = int(vcount % VT);
+            mbar_wait(ve + 8 * slot, ((vcount / VT) & 1) ^ 1);
+            mbar_arrive_expect_tx_w(vf + 8 * slot, C::V_UNIT);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+              tma_load_4d_w(vbuf + slot * C::V_UNIT + c * C::V_ATOM, &tm_v, vf + 8 * slot, c * 64,
+                            j * 128 + hh * 64, g, b, kEvictLast);
+            ++vcount;
           }
-          const uint32_t hb = GT == 2 ? w : (w ? 3u : 0u);  // 64-key halves kept
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            if (((hb & ~prev) >> hh) & 1u) {
-              const int slot = int(vcount % VS);
-              mbar_wait(v_empty + 8 * slot, ((vcount / VS) & 1) ^ 1);
-              mbar_arrive_expect_tx_w(v_full + 8 * slot, C::V_UNIT);
-#pragma unroll
-              for (int c = 0; c < NCH; ++c)
-                tma_load_4d_w(sV + slot * C::V_UNIT + c * C::V_ATOM, &tm_v, v_full + 8 * slot, c * 64,
-                              j * 128 + hh * 64, g, b, kEvictLast);
-              ++vcount;
-            }
-          }
-          prev |= hb;
         }
       }
       if (lane == 0 && p.counters) {
-        // counters in gate tiles: a b_n = 128 gate tile is two 64-key units
+        // in gate tiles: a b_n = 128 gate tile is two 64-key units
         atomicAdd(&p.counters[2], (unsigned long long)(vcount / (3 - GT)));
-        atomicAdd(&p.counters[3], (unsigned long long)nsteps * GT);
+        atomicAdd(&p.counters[3], (unsigned long long)ns * GT);
       }
     }
     __syncwarp();
     named_bar_arrive(15, C::NUM_THREADS);
     return;
-  } else if (warp == C::MMA_WARP || (BSFA_FWD3_SPLIT && warp == C::PV_WARP)) {
+  } else if (warp == C::QK_WARP) {
     setmaxnreg_dec<C::REG_OTHER>();
-    // ======================= tcgen05 issuers (warp-convergent, one elected lane) ========
-    // warp 9 issues the QKs (and owns TMEM), warp 11 the PVs: a QK is issued
-    // as soon as S is free, never queued behind another tile's P hand-off
-    const bool qk_role = warp == C::MMA_WARP;
-    const bool pv_role = !BSFA_FWD3_SPLIT || warp == C::PV_WARP;
+    // ======================= QK issuer (warp-convergent, one elected lane) ============
     if (nsteps > 0) {
       constexpr uint32_t IDESC_QK = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t IDESC_PV = make_idesc_bf16(128, D, 0, 1);
       const uint64_t dq0 = make_sdesc_sw128(sQ, 16, 1024);
       const uint64_t dk0 = make_sdesc_sw128(sK, 16, 1024);
-      const uint64_t dv0 = make_sdesc_sw128(sV, C::V_ATOM, 1024);
       mbar_wait(bar_q, 0);
-
       // S is owned by one tile at a time: every QK after the first waits for
       // the previous owner's tcgen05.ld (one s_free phase per read, in order)
       uint32_t sfree_ph = 0;
-      auto issue_qk = [&](int s, int j) {
-        const unsigned u0 = unsigned(j) * NCH;
-        const bool wait_s = s != 0 || j != 0;
-        if (s == 0) {
-          // tile 0 is the first reader of K(j): S free + every chunk landed, tested together
-          if (NCH == 2 && wait_s)
-            mbar_wait3(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1,
-                       k_full + 8 * int((u0 + 1) % KC), ((u0 + 1) / KC) & 1);
-          else if (wait_s)
-            mbar_wait2(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1);
-          else
-            for (int c = 0; c < NCH; ++c) mbar_wait(k_full + 8 * int((u0 + c) % KC), ((u0 + c) / KC) & 1);
-        } else {
-          mbar_wait(s_free, sfree_ph & 1u);
-        }
-        if (wait_s) ++sfree_ph;
-        if (lane == 0) trace(10, s, j);
-        tc_fence_after();
-        const int last = j < ns_a[1] ? 1 : 0;  // last reader of K(j)
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          const unsigned u = u0 + c;
-          const int slot = int(u % KC);
-          umma_qk_chunk_w(tmem + C::S_COL, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
-                          dk0 + uint64_t((slot * C::K_CHUNK) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
-          if (s == last) umma_commit_w(k_empty + 8 * slot);
-        }
-        umma_commit_w(s_full + 8 * s);
-        if (lane == 0) trace(5, s, j);
-      };
-
-      unsigned vbase = 0;      // V units consumed before this step
-      unsigned nunits = 0;     // V units of the current step
-      uint32_t prev = 0;       // 64-key halves of the current step already given a unit
-      unsigned uidx[2] = {0u, 0u};
-      uint32_t o_started = 0;  // bit s: O_s holds a partial sum
-      auto issue_pv = [&](int s, int j) {
-        const int sb = sbits(j, qi_a[s]);
-        mbar_wait(p_full + 16 * s + 8 * (j & 1), (j >> 1) & 1);
-        tc_fence_after();
-        if (lane == 0) trace(6, s, j);
-        const uint32_t bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + (2 * s + (j & 1)) * 4);
-        const uint32_t hb = GT == 2 ? bits : (bits ? 3u : 0u);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-          if (((hb & ~prev) >> hh) & 1u) uidx[hh] = vbase + nunits++;
-        prev |= hb;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if ((hb >> hh) & 1u) {
-            const unsigned uu = uidx[hh];
-            mbar_wait(v_full + 8 * (uu % VS), (uu / VS) & 1);
-            if (lane == 0) trace(11, s, j);
-            tc_fence_after();
-            umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::P_COL + s * 64 + hh * 32,
-                        dv0 + uint64_t(((uu % VS) * C::V_UNIT) >> 4), IDESC_PV, (o_started >> s) & 1u);
-            o_started |= 1u << s;
-          }
-        }
-        umma_commit_w(pv_done + 8 * s);  // every step: P_s is free again once these PVs land
-        if (j == ns_a[s] - 1) umma_commit_w(o_full + 8 * s);
-        if (lane == 0) trace(7, s, j);
-      };
-
-      if (qk_role) {
-        issue_qk(0, 0);
-        if (ns_a[1] > 0) issue_qk(1, 0);
-      }
       for (int j = 0; j < nsteps; ++j) {
-        prev = 0;
-        nunits = 0;
-        if (qk_role && j + 1 < ns_a[0]) issue_qk(0, j + 1);
-        if (pv_role) issue_pv(0, j);
-        if (qk_role && j + 1 < ns_a[1]) issue_qk(1, j + 1);
-        if (pv_role && j < ns_a[1]) issue_pv(1, j);
-        if (pv_role) {
-          for (unsigned x = 0; x < nunits; ++x) umma_commit_w(v_empty + 8 * ((vbase + x) % VS));
-          vbase += nunits;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (j >= ns_a[s]) continue;
+          const unsigned u0 = unsigned(j) * NCH;
+          const bool wait_s = s != 0 || j != 0;
+          if (s == 0) {  // the first reader of K(j): S free + every chunk landed, tested together
+            if (NCH == 2 && wait_s)
+              mbar_wait3(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1,
+                         k_full + 8 * int((u0 + 1) % KC), ((u0 + 1) / KC) & 1);
+            else if (wait_s)
+              mbar_wait2(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1);
+            else
+              for (int c = 0; c < NCH; ++c) mbar_wait(k_full + 8 * int((u0 + c) % KC), ((u0 + c) / KC) & 1);
+          } else {
+            mbar_wait(s_free, sfree_ph & 1u);
+          }
+          if (wait_s) ++sfree_ph;
+          if (lane == 0) trace(10, s, j);
+          tc_fence_after();
+          const int last = j < ns_a[1] ? 1 : 0;  // last reader of K(j)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            const int slot = int((u0 + c) % KC);
+            umma_qk_chunk_w(tmem + C::S_COL, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
+                            dk0 + uint64_t((slot * C::K_CHUNK) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
+            if (s == last) umma_commit_w(k_empty + 8 * slot);
+          }
+          umma_commit_w(s_full + 8 * s);
+          if (lane == 0) trace(5, s, j);
         }
       }
     }
     __syncwarp();
-    if (!qk_role) {
-      named_bar_arrive(15, C::NUM_THREADS);
-      return;
-    }
     named_bar_sync(15, C::NUM_THREADS);
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
     return;
-  } else if (warp < 8) {
+  } else {
     setmaxnreg_inc<C::REG_SOFT>();
-    // ======================= softmax of query tile s =======================
+    // ======================= softmax of query tile s (+ its PVs) ===================
     const int s = warp >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;
@@ -425,6 +346,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       named_bar_arrive(15, C::NUM_THREADS);
       return;
     }
+    const bool pv_warp = wq == 3;  // issues this tile's PV MMAs
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const uint32_t s_row = tmem + lane_off + C::S_COL;            // the shared score buffer
     const uint32_t p_row = tmem + lane_off + C::P_COL + s * 64;   // this tile's P (bf16 pairs)
@@ -433,6 +355,9 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     const float scale = p.scale;
     const float rescale_raw = p.rescale_raw;
     const int valid_len = p.valid_len;
+    constexpr uint32_t IDESC_PV = make_idesc_bf16(128, D, 0, 1);
+    const uint64_t dv0 = make_sdesc_sw128(sV + s * VT * C::V_UNIT, C::V_ATOM, 1024);
+    const uint32_t vf = v_full + 8 * VT * s, ve = v_empty + 8 * VT * s;
 
     float T = 0.f;
     if constexpr (GM == 0) {
@@ -444,7 +369,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     float m_ref = -INFINITY;   // raw reference max of this row over its kept tiles
     float l_sum = 0.f;         // row sum relative to m_ref
     bool o_valid = false;      // tile-uniform: O_s holds data
-    unsigned dn = 0;
+    unsigned dn = 0;           // voted decisions posted
+    unsigned vcount = 0;       // V units this tile consumed (its producer's order)
+    unsigned npv = 0;          // steps that issued PVs (pv_done phases)
+    bool pv_pending = false;   // the last PV step has not been waited on yet
     unsigned long long kept_tiles = 0;
     int8_t* drow = p.decisions ? p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi_s) * p.gate_cols
                                : nullptr;
@@ -501,8 +429,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         mx[0] = fmaxf(mh[0], mh[1]);
       }
       if (BSFA_TRACE && r == 0) {
-        // keep the clock read after the maxima (a dependent no-op on them)
-        asm volatile("" ::"f"(mx[0]));
+        asm volatile("" ::"f"(mx[0]));  // keep the clock read after the maxima
         trace(8, s, j);
       }
 
@@ -536,17 +463,15 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         asm volatile("" ::"r"(bits));
         trace(9, s, j);
       }
-      // bookkeeping spread over the tile's warps (every thread holds `bits`), so
-      // no single warp lags into the next vote
+      // bookkeeping spread over the tile's warps (every thread holds `bits`)
       if (GM != 1 && r == 64 && sb < 0) {
         // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
-        // few steps at most -- it gates the PVs -- so this never spins in practice)
+        // few steps at most -- it gates this tile's PVs -- so this never spins)
         if (dn >= DQ)
           while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
           }
         st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
       }
-      if (r == 32) sts_u32(decm_sm + (2 * s + (j & 1)) * 4, bits);
       if (r == 96) kept_tiles += __popc(bits);
       if (drow && r == 0) {
 #pragma unroll
@@ -555,10 +480,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
       if (GM != 1 && sb < 0) ++dn;
       if (r == 0) trace(2, s, j);
-      const uint32_t p_bar = p_full + 16 * s + 8 * (j & 1);
       if (bits == 0) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_bar);
         if (r == 0) {
           trace(3, s, j);
           trace(4, s, j);
@@ -581,12 +503,16 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         m_ref = m_new;
         rescale = true;
       }
-      // lazy rescale (reference max moved by more than 2^8): O_s must be
-      // quiescent -- every PV_s up to step j-1 landed
-      bool pv_free = j == 0;  // PV_s(j-1) landed: O_s quiescent, P_s reusable
+      // the tile's last PVs must have landed before O_s is rescaled or P_s rewritten
+      auto pv_wait = [&]() {
+        if (pv_pending) {
+          mbar_wait(pv_done + 8 * s, (npv - 1) & 1);
+          pv_pending = false;
+        }
+      };
+      // lazy rescale (reference max moved by more than 2^8)
       if (__any_sync(0xffffffffu, rescale)) {
-        if (!pv_free) mbar_wait(pv_done + 8 * s, (j - 1) & 1);
-        pv_free = true;
+        pv_wait();
         tc_fence_after();
         const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
@@ -602,7 +528,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           }
           tmem_st32(o_row + c, ov);
         }
-        tmem_wait_st();
       }
 
       // P = exp2(s * scale*log2e - m * scale*log2e) per 64-key half, bf16 pairs
@@ -613,8 +538,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        const bool kept_h = ((hb >> hh) & 1u) != 0;
-        if (kept_h) {
+        if ((hb >> hh) & 1u) {
           uint32_t pk[32];
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
@@ -624,7 +548,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             const float p0 = ex2_approx(f2_lo(x0)), p1 = ex2_approx(f2_hi(x0));
             float p2, p3;
             if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
-              // part of the exponentials on the FMA pipe (relieves the MUFU / MIO queue)
+              // part of the exponentials on the FMA pipe (relieves the MUFU)
               const uint64_t e1 = exp2_poly_x2(ffma2(f2_pack(p0, p1), 0ull, x1));
               p2 = f2_lo(e1);
               p3 = f2_hi(e1);
@@ -637,21 +561,43 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             pk[c / 2] = pack_bf16x2(p0, p1);
             pk[c / 2 + 1] = pack_bf16x2(p2, p3);
           }
-          if (!pv_free) mbar_wait(pv_done + 8 * s, (j - 1) & 1);  // PV_s(j-1) has read P_s
-          pv_free = true;
+          pv_wait();  // the previous PVs of this tile have read P_s
           tmem_st32(p_row + hh * 32, pk);
         }
         if (hh == 0 && r == 0) trace(3, s, j);
       }
       tmem_wait_st();
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_bar);
+      // ---- hand P_s(j) to this tile's PV warp: warps 0-2 arrive, warp 3 waits
+      if (!pv_warp) {
+        named_bar_arrive(5 + s, 128);
+      } else {
+        named_bar_sync(5 + s, 128);
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if ((hb >> hh) & 1u) {
+            const unsigned slot = vcount % VT;
+            mbar_wait(vf + 8 * slot, (vcount / VT) & 1);
+            tc_fence_after();
+            umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::P_COL + s * 64 + hh * 32,
+                        dv0 + uint64_t((slot * C::V_UNIT) >> 4), IDESC_PV, o_valid || hh == 1 && (hb & 1u) ? 1u : 0u);
+            umma_commit_w(ve + 8 * slot);  // the unit is free once this PV landed
+            ++vcount;
+          }
+        }
+        umma_commit_w(pv_done + 8 * s);
+        if (lane == 0) trace(7, s, j);
+      }
+      ++npv;
+      pv_pending = true;
       const uint64_t acc = fadd2(acc0, acc1);
       l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
       o_valid = true;
       if (r == 0) trace(4, s, j);
     }
+    // every PV of this tile landed -> epilogue (one commit covers the warp's MMAs)
+    if (pv_warp) umma_commit_w(o_full + 8 * s);
 
     // ---- epilogue: O = O~ / l, lse = m * scale + ln l (engine.py:178-182)
     mbar_wait(o_full + 8 * s, 0);
@@ -682,10 +628,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       atomicAdd(&p.counters[1], kept_tiles);
     }
     tc_fence_before();
-    named_bar_arrive(15, C::NUM_THREADS);
-    return;
-  } else {
-    setmaxnreg_dec<C::REG_OTHER>();
     named_bar_arrive(15, C::NUM_THREADS);
     return;
   }

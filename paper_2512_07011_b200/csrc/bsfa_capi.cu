@@ -8,10 +8,11 @@
 #include <string>
 
 #include "../../include/bsfa_b200.h"
-#include "bsfa_fwd.cuh"     // K1 v2: per-tile S, all of P in shared memory (also includes bsfa_kernel.cuh)
-#include "bsfa_fwd3.cuh"    // K1 v3: shared S, P in TMEM
-// Forward implementation: 1 = round-1 kernel (TMEM-aliased P half, bsfa_kernel.cuh),
-// 2 = bsfa_fwd.cuh, 3 = bsfa_fwd3.cuh.
+#include "bsfa_fwd3.cuh"    // K1: shared S, P in TMEM (also includes bsfa_kernel.cuh: K2)
+// Forward implementation: 3 = bsfa_fwd3.cuh (production); 1 = the round-1 kernel
+// (TMEM-aliased P half, bsfa_kernel.cuh), built only for A/B timing.  The v2
+// (all of P in shared memory) and v4 (PVs issued by the softmax warps) kernels
+// measured slower and live in experimental/csrc (not built).
 #ifndef BSFA_FWD_IMPL
 #define BSFA_FWD_IMPL 3
 #endif
@@ -116,11 +117,6 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 template <int D, int GT>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
                cudaStream_t st) {
-#if BSFA_FWD_IMPL == 2
-  using C = FCfg<D, GT>;
-  auto kern = bsfa_fwd_kernel<D, GT>;
-  if (int rc = ensure_smem_attr<bsfa_fwd_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
-#else
   using C = FCfg3<D, GT>;
   // gate class and causality are template parameters of the v3 kernel
   const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
@@ -139,7 +135,6 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   BSFA_GM(2, false)
 #undef BSFA_GM
   if (rc) return rc;
-#endif
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
