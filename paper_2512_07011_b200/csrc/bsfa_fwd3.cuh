@@ -132,7 +132,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   // the softmax's critical path; dec_cons[s] = decisions the producer consumed
   const uint32_t dec_sm = sbase + C::OFF_DEC;
   const uint32_t dec_cons = sbase + C::OFF_DECC;
-  const uint32_t decm_sm = sbase + C::OFF_DECM;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -358,12 +357,24 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       uint32_t prev = 0;       // 64-key halves of the current step already given a unit
       unsigned uidx[2] = {0u, 0u};
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
+      unsigned dn_m[2] = {0u, 0u};                // voted decisions read, per tile
+      unsigned long long kept_m = 0;              // processed gate tiles (counters[1])
       auto issue_pv = [&](int s, int j) {
         const int sb = sbits(j, qi_a[s]);
         mbar_wait(p_full + 16 * s + 8 * (j & 1), (j >> 1) & 1);
         tc_fence_after();
         if (lane == 0) trace(6, s, j);
-        const uint32_t bits = sb >= 0 ? uint32_t(sb) : lds_u32(decm_sm + (2 * s + (j & 1)) * 4);
+        uint32_t bits;
+        if (sb >= 0) {
+          bits = uint32_t(sb);
+        } else {
+          // the tile's decision was posted to its tagged ring before its p_full
+          // arrivals; the ring slot is reused only DQ voted steps later
+          const unsigned n = s ? dn_m[1] : dn_m[0];
+          bits = ld_volatile_u32(dec_sm + (s * DQ + int(n % DQ)) * 4) & 0xFu;
+          if (s) ++dn_m[1]; else ++dn_m[0];
+        }
+        kept_m += __popc(bits);
         const uint32_t hb = GT == 2 ? bits : (bits ? 3u : 0u);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
@@ -401,6 +412,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           for (unsigned x = 0; x < nunits; ++x) umma_commit_w(v_empty + 8 * ((vbase + x) % VS));
           vbase += nunits;
         }
+      }
+      if (pv_role && lane == 0 && p.counters) {
+        atomicAdd(&p.counters[0], (unsigned long long)(ns_a[0] + ns_a[1]) * GT);
+        atomicAdd(&p.counters[1], kept_m);
       }
     }
     __syncwarp();
@@ -445,7 +460,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     float l_sum = 0.f;         // row sum relative to m_ref
     bool o_valid = false;      // tile-uniform: O_s holds data
     unsigned dn = 0;
-    unsigned long long kept_tiles = 0;
     int8_t* drow = p.decisions ? p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi_s) * p.gate_cols
                                : nullptr;
 
@@ -546,8 +560,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           }
         st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
       }
-      if (r == 32) sts_u32(decm_sm + (2 * s + (j & 1)) * 4, bits);
-      if (r == 96) kept_tiles += __popc(bits);
       if (drow && r == 0) {
 #pragma unroll
         for (int x = 0; x < GT; ++x)
@@ -677,10 +689,6 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
     p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
     if (bad && p.status) atomicOr(p.status, 1);
-    if (r == 96 && p.counters) {
-      atomicAdd(&p.counters[0], (unsigned long long)nst * GT);
-      atomicAdd(&p.counters[1], kept_tiles);
-    }
     tc_fence_before();
     named_bar_arrive(15, C::NUM_THREADS);
     return;
