@@ -550,7 +550,8 @@ def test_negative_control_corrupted_v_tile(bsfa):
 
     The decisions do not depend on V, so the oracle replays the same mask on the
     clean V; rows that kept the corrupted tile must exceed ROW_RTOL while the
-    clean run stays inside it (engine.py:157-182: a kept tile enters every such row).
+    clean run stays inside it (engine.py:157-182: a kept tile enters every such
+    row) -- and the corruption is small enough that max-abs <= ATOL alone misses it.
     """
     n, d = 32768, 128
     gen = torch.Generator(device="cuda").manual_seed(77)
@@ -564,7 +565,7 @@ def test_negative_control_corrupted_v_tile(bsfa):
     j_bad = 100  # an off-frontier gate tile kept by many query blocks
     assert np.count_nonzero(dec[:, j_bad] == orc.KEPT) > 50
     v_bad = v.clone()
-    v_bad[0, 0, j_bad * 64:(j_bad + 1) * 64] += 1.0
+    v_bad[0, 0, j_bad * 64:(j_bad + 1) * 64] += 0.25  # small enough that max-abs stays under ATOL
     bad = bsfa.attention(q, k, v_bad, thresholds=t, k_level=1, return_trace=True)
     assert torch.equal(bad.decisions, res.decisions)
     qh, kh, vh = (x[0, 0].float().cpu().numpy() for x in (q, k, v))
@@ -578,7 +579,7 @@ def test_negative_control_corrupted_v_tile(bsfa):
     assert clean <= ROW_RTOL, clean
     assert corrupt > 5 * ROW_RTOL, corrupt
     # the absolute north_star bound alone would not have noticed
-    assert np.abs(bad.o[0, 0].float().cpu().numpy() - o_ref).max() <= 0.5
+    assert np.abs(bad.o[0, 0].float().cpu().numpy() - o_ref).max() <= ATOL
 
 
 def test_llama_128k_sampled_heads(bsfa):
