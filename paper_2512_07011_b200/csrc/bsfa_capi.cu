@@ -8,15 +8,10 @@
 #include <string>
 
 #include "../../include/bsfa_b200.h"
-#include "bsfa_fwd3.cuh"    // K1: shared S, P in TMEM (also includes bsfa_kernel.cuh: K2)
-// Forward implementation: 3 = bsfa_fwd3.cuh (production); 1 = the round-1 kernel
-// (TMEM-aliased P half, bsfa_kernel.cuh), built only for A/B timing.  The v2
-// (all of P in shared memory) and v4 (PVs issued by the softmax warps) kernels
-// measured slower and live in experimental/csrc (not built).
-#ifndef BSFA_FWD_IMPL
-#define BSFA_FWD_IMPL 3
-#endif
-#define BSFA_FWD_V1 (BSFA_FWD_IMPL == 1)
+#include "bsfa_calib.cuh"    // K2: calibration block maxima + cutoffs
+#include "bsfa_fwd3.cuh"     // K1: forward (shared S, P in TMEM)
+// The round-1 forward and the other measured alternatives live in
+// experimental/csrc (not built); DESIGN.md section 5 has their numbers.
 
 static_assert(BSFA_MAX_O_PEERS == sizeof(bsfa::KernelParams::o_peer) / sizeof(void*), "peer slots");
 
@@ -99,17 +94,16 @@ int ensure_smem_attr(int bytes) {
   return BSFA_OK;
 }
 
-// calibration kernel K2 (and, with -DBSFA_FWD_V1=1, the round-1 forward)
-template <int D, int GT, int NQ, bool CALIB>
-int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
-           cudaStream_t st) {
-  using C = KCfg<D, GT, NQ, CALIB, 1>;
-  auto kern = bsfa_kernel<D, GT, NQ, CALIB, 1>;
-  if (int rc = ensure_smem_attr<bsfa_kernel<D, GT, NQ, CALIB, 1>>(C::SMEM_BYTES)) return rc;
+// calibration kernel K2 (bsfa_calib.cuh)
+template <int D, int GT>
+int launch_calib(const CUtensorMap& tq, const CUtensorMap& tk, const KernelParams& p, int grid, cudaStream_t st) {
+  using C = CCfg<D, GT>;
+  auto kern = bsfa_calib_kernel<D, GT>;
+  if (int rc = ensure_smem_attr<bsfa_calib_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
   if (grid == 0) return BSFA_OK;
-  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, p);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "bsfa kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa calibration launch");
   return BSFA_OK;
 }
 
@@ -142,27 +136,28 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   return BSFA_OK;
 }
 
-template <bool CALIB>
-int dispatch(int d, int b_n, int nq, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-             const KernelParams& p, int grid, cudaStream_t st) {
-  if constexpr (!CALIB && !BSFA_FWD_V1) {
+int dispatch_fwd(int d, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                 const KernelParams& p, int grid, cudaStream_t st) {
 #define BSFA_FWD(D_, BN_) \
   if (d == D_ && b_n == BN_) return launch_fwd<D_, 128 / BN_>(tq, tk, tv, p, grid, st);
-    BSFA_FWD(64, 64)
-    BSFA_FWD(128, 64)
-    BSFA_FWD(64, 128)
-    BSFA_FWD(128, 128)
+  BSFA_FWD(64, 64)
+  BSFA_FWD(128, 64)
+  BSFA_FWD(64, 128)
+  BSFA_FWD(128, 128)
 #undef BSFA_FWD
-    return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
-  }
-#define BSFA_CASE(D_, BN_, NQ_) \
-  if (d == D_ && b_n == BN_ && nq == NQ_) return launch<D_, 128 / BN_, NQ_, CALIB>(tq, tk, tv, p, grid, st);
-  BSFA_CASE(64, 64, 2)
-  BSFA_CASE(128, 64, 2)
-  BSFA_CASE(64, 128, 2)
-  BSFA_CASE(128, 128, 2)
-#undef BSFA_CASE
   return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
+}
+
+int dispatch_calib(int d, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const KernelParams& p, int grid,
+                   cudaStream_t st) {
+#define BSFA_CAL(D_, BN_) \
+  if (d == D_ && b_n == BN_) return launch_calib<D_, 128 / BN_>(tq, tk, p, grid, st);
+  BSFA_CAL(64, 64)
+  BSFA_CAL(128, 64)
+  BSFA_CAL(64, 128)
+  BSFA_CAL(128, 128)
+#undef BSFA_CAL
+  return fail(BSFA_ERR_INVALID, "no calibration kernel for head_dim=%d b_n=%d", d, b_n);
 }
 
 int check_tiles(int b_m, int b_n) {
@@ -232,7 +227,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b,
-                   BSFA_FWD_V1 ? a->b_n : 64, "v"))
+                   64, "v"))
     return rc;
 
   KernelParams p;
@@ -282,7 +277,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   const long long grid = p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
-  return dispatch<false>(d, a->b_n, nq, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  (void)nq;
+  return dispatch_fwd(d, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
@@ -294,8 +290,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
     return fail(BSFA_ERR_INVALID, "seq_len %d must be a positive multiple of 128 (pad first)", a->seq_len);
-  if (a->seq_len / a->b_n > KCfg<64, 2, 1, true>::MAXA)
-    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", KCfg<64, 2, 1, true>::MAXA);
+  if (a->seq_len / a->b_n > CCfg<64, 2>::MAXA)
+    return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", CCfg<64, 2>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
   if (a->seq_len / a->b_m > a->num_positions)
@@ -343,7 +339,8 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.block_pair = p.group % 2 == 1 ? 1 : 0;
   const int nq = 2;
   const int grid = p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2) : (a->heads_q / nq) * p.num_q_tiles;
-  return dispatch<true>(d, a->b_n, nq, tq, tk, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+  (void)nq;
+  return dispatch_calib(d, a->b_n, tq, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

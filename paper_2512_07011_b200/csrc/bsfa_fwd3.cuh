@@ -40,7 +40,7 @@
 // 64-key half.
 #pragma once
 
-#include "bsfa_kernel.cuh"
+#include "bsfa_common.cuh"
 
 #ifndef BSFA_FWD3_KC
 #define BSFA_FWD3_KC 0  // 0: default per head_dim
