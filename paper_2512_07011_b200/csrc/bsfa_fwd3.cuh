@@ -51,6 +51,11 @@
 // 1: QKs issued by warp 9, PVs by warp 11 (each waits only on its own inputs;
 // measured 20 % slower: PVs then queue behind QKs in the in-order tensor pipe);
 // 0: one issuer in the order QK_0(j+1) PV_0(j) QK_1(j+1) PV_1(j)
+// ThresholdGate vote at b_n = 64: 1 = one barrier for both gate tiles of a step
+// (warp REDUX + shared words), 0 = one BAR.RED.OR per gate tile
+#ifndef BSFA_VOTE1
+#define BSFA_VOTE1 1
+#endif
 #ifndef BSFA_FWD3_SPLIT
 #define BSFA_FWD3_SPLIT 0
 #endif
@@ -79,8 +84,8 @@ struct FCfg3 {
   static constexpr int OFF_DEC = (OFF_BAR + NUM_BARS * 8 + 15) / 16 * 16;  // u32 [2][DQ] tagged decisions
   static constexpr int OFF_DECC = OFF_DEC + 2 * DQ * 4;                    // u32 [2] decisions consumed
   static constexpr int OFF_DECM = OFF_DECC + 2 * 4;                        // u32 [2][2 parity]
-  static constexpr int OFF_XCH = OFF_DECM + 4 * 4;                         // f32 [2][128] epilogue
-  static constexpr int OFF_TMEMPTR = OFF_XCH + 2 * 128 * 4;
+  static constexpr int OFF_VOTE = (OFF_DECM + 4 * 4 + 15) / 16 * 16;      // u32 [2][2 parity][4 warps]
+  static constexpr int OFF_TMEMPTR = OFF_VOTE + 2 * 2 * 4 * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   static constexpr int O_COL = 0;          // O_s at s * D
   static constexpr int S_COL = 2 * D;      // the shared score buffer
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   // the softmax's critical path; dec_cons[s] = decisions the producer consumed
   const uint32_t dec_sm = sbase + C::OFF_DEC;
   const uint32_t dec_cons = sbase + C::OFF_DECC;
+  const uint32_t vote_sm = sbase + C::OFF_VOTE;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -526,9 +532,23 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         bits = uint32_t(sb);
       } else if constexpr (GM == 0) {
         // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
-        bits = 0;
+        if constexpr (GT == 2 && BSFA_VOTE1) {
+          // both gate tiles in ONE barrier: OR within the warp (REDUX), one word
+          // per warp in shared memory (parity double-buffered: a warp reaches
+          // step j+2's store only after every warp passed step j+1's barrier,
+          // i.e. read step j's words), bar.sync, OR of the four words
+          const uint32_t v = (mx[0] * scale > T ? 1u : 0u) | (mx[1] * scale > T ? 2u : 0u);
+          const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
+          const uint32_t slot = vote_sm + (s * 2 + (j & 1)) * 16;
+          if (lane == 0) sts_u32(slot + wq * 4, wv);
+          named_bar_sync(1 + s, 128);
+          const uint4 all = lds_u128(slot);
+          bits = all.x | all.y | all.z | all.w;
+        } else {
+          bits = 0;
 #pragma unroll
-        for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
+          for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
+        }
       } else {
         // RunningMaxGate (gates.py:101-118): gate tiles in key order, each judged
         // against the running max before it is merged
