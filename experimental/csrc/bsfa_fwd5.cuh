@@ -1,5 +1,6 @@
-// BSFA forward (K1) for sm_100a, v3: one score buffer shared by the two query
-// tiles, P in tensor memory.
+// BSFA forward (K1) for sm_100a, v5: one score buffer PER query tile (QK_s(j+1)
+// issued as soon as tile s read S_s(j)), all of P in shared memory (SS-form PV).
+// Otherwise as v3 (bsfa_fwd3.cuh): templates, tagged decision ring, one-barrier vote.
 //
 // One CTA owns two query tiles (128 rows each) that read the same K/V: two q
 // heads of one GQA group at query block i, or -- odd groups, MHA -- query
@@ -42,21 +43,17 @@
 
 #include "bsfa_common.cuh"
 
-#ifndef BSFA_FWD3_KC
-#define BSFA_FWD3_KC 0  // 0: default per head_dim
+#ifndef BSFA_FWD5_KC
+#define BSFA_FWD5_KC 0  // 0: default per head_dim
 #endif
-#ifndef BSFA_FWD3_VS
-#define BSFA_FWD3_VS 0
+#ifndef BSFA_FWD5_VS
+#define BSFA_FWD5_VS 0
 #endif
 // 1: QKs issued by warp 9, PVs by warp 11 (each waits only on its own inputs;
 // measured 20 % slower: PVs then queue behind QKs in the in-order tensor pipe);
 // 0: one issuer in the order QK_0(j+1) PV_0(j) QK_1(j+1) PV_1(j)
 // ThresholdGate vote at b_n = 64: 1 = one barrier for both gate tiles of a step
 // (warp REDUX + shared words), 0 = one BAR.RED.OR per gate tile
-// with BSFA_EXP_EMU: make each polynomial pair depend on the preceding MUFU pair
-#ifndef BSFA_EXP_CHAIN
-#define BSFA_EXP_CHAIN 1
-#endif
 #ifndef BSFA_VOTE1
 #define BSFA_VOTE1 1
 #endif
@@ -67,7 +64,7 @@
 namespace bsfa {
 
 template <int D, int GT>
-struct FCfg3 {
+struct FCfg5 {
   static constexpr int BN = 128 / GT;           // gate tile width (reference b_n)
   static constexpr int NCH = D / 64;            // 64-column swizzle atoms along head_dim
   static constexpr int Q_TILE = 128 * D * 2;
@@ -75,13 +72,16 @@ struct FCfg3 {
   static constexpr int K_CHUNK = 128 * 128;     // 128 keys x 64 columns, bf16
   static constexpr int V_UNIT = 64 * D * 2;     // 64 keys of V
   static constexpr int V_ATOM = 64 * 128;       // 64 keys x 64 columns
-  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : 4;
-  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 128 ? 6 : 8);
+  static constexpr int KC = BSFA_FWD5_KC ? BSFA_FWD5_KC : (D == 128 ? 2 : 4);
+  static constexpr int VS = BSFA_FWD5_VS ? BSFA_FWD5_VS : (D == 128 ? 4 : 6);
+  static constexpr int P_HALF = 128 * 128;      // 128 rows x 64 keys, bf16 (one SW128 atom column)
+  static constexpr int P_TILE = 2 * P_HALF;
   static constexpr int DQ = 8;                  // decision ring depth (V producer)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
   static constexpr int OFF_V = OFF_K + KC * K_CHUNK;
-  static constexpr int OFF_BAR = OFF_V + VS * V_UNIT;
+  static constexpr int OFF_P = OFF_V + VS * V_UNIT;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_TILE;
   // bar_q, k_full/empty[KC], v_full/empty[VS], s_full[2], s_free,
   // p_full[2][2 parity], pv_done[2], o_full[2]
   static constexpr int NUM_BARS = 1 + 2 * KC + 2 * VS + 2 + 2 + 4 + 2 + 2;
@@ -92,8 +92,7 @@ struct FCfg3 {
   static constexpr int OFF_TMEMPTR = OFF_VOTE + 2 * 2 * 4 * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   static constexpr int O_COL = 0;          // O_s at s * D
-  static constexpr int S_COL = 2 * D;      // the shared score buffer
-  static constexpr int P_COL = S_COL + 128;  // P_s (bf16 pairs) at P_COL + s * 64
+  static constexpr int S_COL = 2 * D;      // S_s at S_COL + s * 128
   static constexpr int TMEM_COLS = 512;
   static constexpr int NUM_THREADS = 12 * 32;
   static constexpr int KPROD_WARP = 8, MMA_WARP = 9, VPROD_WARP = 10, PV_WARP = 11;
@@ -103,7 +102,7 @@ struct FCfg3 {
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
   static_assert(D == 64 || D == 128, "head_dim 64 or 128");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-  static_assert(P_COL + 128 <= TMEM_COLS, "TMEM budget");
+  static_assert(S_COL + 256 <= TMEM_COLS, "TMEM budget");
   static_assert(KC >= NCH + 1 || KC >= 2, "K ring");
   static_assert(VS >= 2, "V ring must hold one step");
 };
@@ -113,10 +112,10 @@ struct FCfg3 {
 // CAUSAL are template parameters so the per-step softmax code carries no
 // runtime gate/causality branches (smaller loop body, fewer taken branches).
 template <int D, int GT, int GM, bool CAUSAL>
-__global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
-    bsfa_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+__global__ void __launch_bounds__(FCfg5<D, GT>::NUM_THREADS, 1)
+    bsfa_fwd5_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = FCfg3<D, GT>;
+  using C = FCfg5<D, GT>;
   constexpr int KC = C::KC, VS = C::VS, DQ = C::DQ, NCH = C::NCH;
 
   extern __shared__ uint8_t smem_raw[];
@@ -126,13 +125,14 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   const uint32_t sQ = sbase + C::OFF_Q;
   const uint32_t sK = sbase + C::OFF_K;
   const uint32_t sV = sbase + C::OFF_V;
+  const uint32_t sP = sbase + C::OFF_P;
   const uint32_t bar_q = sbase + C::OFF_BAR;
   const uint32_t k_full = bar_q + 8;
   const uint32_t k_empty = k_full + 8 * KC;
   const uint32_t v_full = k_empty + 8 * KC;
   const uint32_t v_empty = v_full + 8 * VS;
   const uint32_t s_full = v_empty + 8 * VS;    // [2]  QK_s(j) landed in S
-  const uint32_t s_free = s_full + 16;         // the tile that owned S copied it to registers (4 warps)
+  const uint32_t s_free = s_full + 16;         // [2]  tile s copied S_s to registers (4 warps)
   const uint32_t p_full = s_free + 16;         // [2][2 parity]  P_s(j) written / step decided (4 warps)
   const uint32_t pv_done = p_full + 32;        // [2]  PV_s(j) landed (every step): P_s is free again
   const uint32_t o_full = pv_done + 16;        // [2]  last PV_s landed
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(s_full + 8 * s, 1);
-      if (s == 0) mbar_init(s_free, 4);
+      mbar_init(s_free + 8 * s, 4);
       mbar_init(p_full + 16 * s, 4);
       mbar_init(p_full + 16 * s + 8, 4);
       mbar_init(pv_done + 8 * s, 1);
@@ -326,27 +326,26 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       const uint64_t dq0 = make_sdesc_sw128(sQ, 16, 1024);
       const uint64_t dk0 = make_sdesc_sw128(sK, 16, 1024);
       const uint64_t dv0 = make_sdesc_sw128(sV, C::V_ATOM, 1024);
+      const uint64_t dp0 = make_sdesc_sw128(sP, 16, 1024);
       mbar_wait(bar_q, 0);
 
-      // S is owned by one tile at a time: every QK after the first waits for
-      // the previous owner's tcgen05.ld (one s_free phase per read, in order)
-      uint32_t sfree_ph = 0;
+      // QK_s(j) needs tile s to have read S_s(j-1) (s_free phase j-1)
       auto issue_qk = [&](int s, int j) {
         const unsigned u0 = unsigned(j) * NCH;
-        const bool wait_s = s != 0 || j != 0;
+        const bool wait_s = j != 0;
+        const uint32_t sf = s_free + 8 * s, sfp = (j - 1) & 1;
         if (s == 0) {
           // tile 0 is the first reader of K(j): S free + every chunk landed, tested together
           if (NCH == 2 && wait_s)
-            mbar_wait3(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1,
-                       k_full + 8 * int((u0 + 1) % KC), ((u0 + 1) / KC) & 1);
+            mbar_wait3(sf, sfp, k_full + 8 * int(u0 % KC), (u0 / KC) & 1, k_full + 8 * int((u0 + 1) % KC),
+                       ((u0 + 1) / KC) & 1);
           else if (wait_s)
-            mbar_wait2(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1);
+            mbar_wait2(sf, sfp, k_full + 8 * int(u0 % KC), (u0 / KC) & 1);
           else
             for (int c = 0; c < NCH; ++c) mbar_wait(k_full + 8 * int((u0 + c) % KC), ((u0 + c) / KC) & 1);
-        } else {
-          mbar_wait(s_free, sfree_ph & 1u);
+        } else if (wait_s) {
+          mbar_wait(sf, sfp);
         }
-        if (wait_s) ++sfree_ph;
         if (lane == 0) trace(10, s, j);
         tc_fence_after();
         const int last = j < ns_a[1] ? 1 : 0;  // last reader of K(j)
@@ -354,7 +353,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         for (int c = 0; c < NCH; ++c) {
           const unsigned u = u0 + c;
           const int slot = int(u % KC);
-          umma_qk_chunk_w(tmem + C::S_COL, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
+          umma_qk_chunk_w(tmem + C::S_COL + s * 128, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
                           dk0 + uint64_t((slot * C::K_CHUNK) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
           if (s == last) umma_commit_w(k_empty + 8 * slot);
         }
@@ -397,8 +396,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             mbar_wait(v_full + 8 * (uu % VS), (uu / VS) & 1);
             if (lane == 0) trace(11, s, j);
             tc_fence_after();
-            umma_pv64_w(tmem + C::O_COL + s * D, tmem + C::P_COL + s * 64 + hh * 32,
-                        dv0 + uint64_t(((uu % VS) * C::V_UNIT) >> 4), IDESC_PV, (o_started >> s) & 1u);
+            umma_pv64_ss_w(tmem + C::O_COL + s * D, dp0 + uint64_t((s * C::P_TILE + hh * C::P_HALF) >> 4),
+                           dv0 + uint64_t(((uu % VS) * C::V_UNIT) >> 4), IDESC_PV, (o_started >> s) & 1u);
             o_started |= 1u << s;
           }
         }
@@ -415,8 +414,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         prev = 0;
         nunits = 0;
         if (qk_role && j + 1 < ns_a[0]) issue_qk(0, j + 1);
-        if (pv_role) issue_pv(0, j);
         if (qk_role && j + 1 < ns_a[1]) issue_qk(1, j + 1);
+        if (pv_role) issue_pv(0, j);
         if (pv_role && j < ns_a[1]) issue_pv(1, j);
         if (pv_role) {
           for (unsigned x = 0; x < nunits; ++x) umma_commit_w(v_empty + 8 * ((vbase + x) % VS));
@@ -451,8 +450,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       return;
     }
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    const uint32_t s_row = tmem + lane_off + C::S_COL;            // the shared score buffer
-    const uint32_t p_row = tmem + lane_off + C::P_COL + s * 64;   // this tile's P (bf16 pairs)
+    const uint32_t s_row = tmem + lane_off + C::S_COL + s * 128;  // this tile's score buffer
+    const uint32_t p_row = sP + s * C::P_TILE + r * 128;           // this row of P_s in shared memory
     const uint32_t o_row = tmem + lane_off + C::O_COL + s * D;
     const float sl2 = p.scale_log2;
     const float scale = p.scale;
@@ -483,7 +482,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);  // the other tile's QK may overwrite S
+      if (lane == 0) mbar_arrive(s_free + 8 * s);  // QK_s(j+1) may overwrite S_s
       if (r == 0) trace(1, s, j);
 
       const int sb = sbits(j, qi_s);
@@ -661,7 +660,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             float p2, p3;
             if (BSFA_EXP_EMU == 2 || (BSFA_EXP_EMU == 1 && ((c >> 2) & 1))) {
               // part of the exponentials on the FMA pipe (relieves the MUFU / MIO queue)
-              const uint64_t e1 = exp2_poly_x2(BSFA_EXP_CHAIN ? ffma2(f2_pack(p0, p1), 0ull, x1) : x1);
+              const uint64_t e1 = exp2_poly_x2(ffma2(f2_pack(p0, p1), 0ull, x1));
               p2 = f2_lo(e1);
               p3 = f2_hi(e1);
             } else {
@@ -675,11 +674,16 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           }
           if (!pv_free) mbar_wait(pv_done + 8 * s, (j - 1) & 1);  // PV_s(j-1) has read P_s
           pv_free = true;
-          tmem_st32(p_row + hh * 32, pk);
+          // K-major SW128: 16-byte chunk c of row r at chunk c ^ (r & 7)
+#pragma unroll
+          for (int c16 = 0; c16 < 8; ++c16)
+            sts_u128(p_row + hh * C::P_HALF + ((c16 ^ (r & 7)) << 4), pk[4 * c16], pk[4 * c16 + 1],
+                     pk[4 * c16 + 2], pk[4 * c16 + 3]);
         }
         if (hh == 0 && r == 0) trace(3, s, j);
       }
-      tmem_wait_st();
+      tmem_wait_st();               // (the O rescale's tcgen05.st)
+      fence_proxy_async_smem();     // generic-proxy P stores -> visible to the tensor core
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_bar);

@@ -116,6 +116,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) = nullptr;
   int rc = BSFA_OK;
+  const int smem = C::SMEM_BYTES;
 #define BSFA_GM(GM_, CA_)                                                                     \
   if (gm == GM_ && (p.causal != 0) == CA_) {                                                  \
     kern = bsfa_fwd3_kernel<D, GT, GM_, CA_>;                                                 \
@@ -130,7 +131,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
 #undef BSFA_GM
   if (rc) return rc;
   if (grid == 0) return BSFA_OK;
-  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  kern<<<grid, C::NUM_THREADS, smem, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bsfa forward launch");
   return BSFA_OK;
