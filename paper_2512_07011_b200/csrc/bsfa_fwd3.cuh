@@ -60,6 +60,11 @@
 #ifndef BSFA_VOTE1
 #define BSFA_VOTE1 1
 #endif
+// with BSFA_VOTE1 (ThresholdGate, b_n = 64): the V producer joins the vote
+// barrier and reads the decision from the vote words itself (no decision ring)
+#ifndef BSFA_VOTE_PRODUCER
+#define BSFA_VOTE_PRODUCER 1
+#endif
 #ifndef BSFA_FWD3_SPLIT
 #define BSFA_FWD3_SPLIT 0
 #endif
@@ -187,6 +192,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   const int gate_mode = p.gate_mode;
   const int window = p.gate_window;
   // statically known decision bits of step j for query block qi (-1: voted)
+  // the V producer reads ThresholdGate decisions straight from the vote words
+  constexpr bool VP = GM == 0 && GT == 2 && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
   auto sbits = [&](int j, int qi) -> int {
     if constexpr (GM == 1) return step_static_bits<GT>(gate_mode, window, j, qi);
     return j == qi ? (1 << GT) - 1 : -1;  // frontier (tiling.py:50-60)
@@ -277,6 +284,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           uint32_t w;
           if (sbs >= 0) {
             w = uint32_t(sbs);
+          } else if constexpr (VP) {
+            named_bar_sync(1 + s, 160);  // the tile's vote (128 softmax threads + this warp)
+            const uint4 all = lds_u128(vote_sm + (s * 2 + (j & 1)) * 16);
+            w = all.x | all.y | all.z | all.w;
           } else {
             const uint32_t slot_addr = dec_sm + (s * DQ + int(dn_a[s] % DQ)) * 4;
             const uint32_t tag = dn_a[s] + 1;
@@ -377,6 +388,11 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         uint32_t bits;
         if (sb >= 0) {
           bits = uint32_t(sb);
+        } else if constexpr (VP) {
+          // the vote words of step j: rewritten only at step j + 2, whose vote
+          // needs QK_s(j+2), issued after this PV
+          const uint4 all = lds_u128(vote_sm + (s * 2 + (j & 1)) * 16);
+          bits = all.x | all.y | all.z | all.w;
         } else {
           // the tile's decision was posted to its tagged ring before its p_full
           // arrivals; the ring slot is reused only DQ voted steps later
@@ -545,7 +561,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
           const uint32_t slot = vote_sm + (s * 2 + (j & 1)) * 16;
           if (lane == 0) sts_u32(slot + wq * 4, wv);
-          named_bar_sync(1 + s, 128);
+          named_bar_sync(1 + s, VP ? 160 : 128);
           const uint4 all = lds_u128(slot);
           bits = all.x | all.y | all.z | all.w;
         } else {
@@ -576,7 +592,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
       // bookkeeping spread over the tile's warps (every thread holds `bits`), so
       // no single warp lags into the next vote
-      if (GM != 1 && r == 64 && sb < 0) {
+      if (GM != 1 && !VP && r == 64 && sb < 0) {
         // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
         // few steps at most -- it gates the PVs -- so this never spins in practice)
         if (dn >= DQ)
