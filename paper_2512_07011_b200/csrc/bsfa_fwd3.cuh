@@ -57,6 +57,9 @@
 #ifndef BSFA_EXP_CHAIN
 #define BSFA_EXP_CHAIN 1
 #endif
+#ifndef BSFA_PV_EVERY_PHASE
+#define BSFA_PV_EVERY_PHASE 0
+#endif
 #ifndef BSFA_VOTE1
 #define BSFA_VOTE1 1
 #endif
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   const uint32_t s_full = v_empty + 8 * VS;    // [2]  QK_s(j) landed in S
   const uint32_t s_free = s_full + 16;         // the tile that owned S copied it to registers (4 warps)
   const uint32_t p_full = s_free + 16;         // [2][2 parity]  P_s(j) written / step decided (4 warps)
-  const uint32_t pv_done = p_full + 32;        // [2]  PV_s(j) landed (every step): P_s is free again
+  const uint32_t pv_done = p_full + 32;        // [2]  the PVs of tile s's last kept step landed
   const uint32_t o_full = pv_done + 16;        // [2]  last PV_s landed
   // decision hand-off to the V producer: tagged words ((n + 1) << 4 | bits) in a
   // DQ ring per tile, polled with volatile loads -- no mbarrier round trips on
@@ -418,7 +421,13 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             o_started |= 1u << s;
           }
         }
-        umma_commit_w(pv_done + 8 * s);  // every step: P_s is free again once these PVs land
+        // P_s is free again once these PVs land.  Default: one pv_done phase per
+        // step; the softmax waits only for the phase before a P write (a skipped
+        // phase is provably complete by then: its commit precedes QK_s(j+1), whose
+        // completion the softmax already waited for).  BSFA_PV_EVERY_PHASE: one
+        // phase per step that issued PVs, each with a waiter (compute-sanitizer
+        // synccheck reports skipped phases as "missing wait").
+        if (!BSFA_PV_EVERY_PHASE || hb) umma_commit_w(pv_done + 8 * s);
         if (j == ns_a[s] - 1) umma_commit_w(o_full + 8 * s);
         if (lane == 0) trace(7, s, j);
       };
@@ -485,11 +494,23 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     float m_ref = -INFINITY;   // raw reference max of this row over its kept tiles
     float l_sum = 0.f;         // row sum relative to m_ref
     bool o_valid = false;      // tile-uniform: O_s holds data
+    unsigned npv = 0;          // steps of this tile that issued PVs (pv_done phases)
+    bool pv_pending = false;   // the last of them not yet waited on
+    auto pv_wait = [&]() {
+      if (pv_pending) {
+        mbar_wait(pv_done + 8 * s, (npv - 1) & 1);
+        pv_pending = false;
+      }
+    };
     unsigned dn = 0;
     int8_t* drow = p.decisions ? p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi_s) * p.gate_cols
                                : nullptr;
 
     for (int j = 0; j < nst; ++j) {
+      if (!BSFA_PV_EVERY_PHASE) {  // default: phase j-1 (step j-1's commit) is the one to wait for
+        npv = unsigned(j);
+        pv_pending = j > 0;
+      }
       mbar_wait(s_full + 8 * s, j & 1);
       if (r == 0) trace(0, s, j);
       tc_fence_after();
@@ -635,10 +656,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
       // lazy rescale (reference max moved by more than 2^8): O_s must be
       // quiescent -- every PV_s up to step j-1 landed
-      bool pv_free = j == 0;  // PV_s(j-1) landed: O_s quiescent, P_s reusable
       if (__any_sync(0xffffffffu, rescale)) {
-        if (!pv_free) mbar_wait(pv_done + 8 * s, (j - 1) & 1);
-        pv_free = true;
+        pv_wait();  // O_s quiescent
         tc_fence_after();
         const uint64_t ax2 = f2_pack(alpha, alpha);
 #pragma unroll
@@ -689,8 +708,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             pk[c / 2] = pack_bf16x2(p0, p1);
             pk[c / 2 + 1] = pack_bf16x2(p2, p3);
           }
-          if (!pv_free) mbar_wait(pv_done + 8 * s, (j - 1) & 1);  // PV_s(j-1) has read P_s
-          pv_free = true;
+          pv_wait();  // the last PVs have read P_s
           tmem_st32(p_row + hh * 32, pk);
         }
         if (hh == 0 && r == 0) trace(3, s, j);
@@ -699,6 +717,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_bar);
+      if (BSFA_PV_EVERY_PHASE) {  // this step issued PVs: one more pv_done phase
+        ++npv;
+        pv_pending = true;
+      }
       const uint64_t acc = fadd2(acc0, acc1);
       l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
       o_valid = true;
@@ -706,6 +728,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     }
 
     // ---- epilogue: O = O~ / l, lse = m * scale + ln l (engine.py:178-182)
+    if (BSFA_PV_EVERY_PHASE) pv_wait();  // (implied by o_full; gives the last phase a waiter)
     mbar_wait(o_full + 8 * s, 0);
     tc_fence_after();
     const float inv_l = 1.f / l_sum;
