@@ -23,6 +23,9 @@
  *                         calibration.py:185-196.
  *   bsfa_calib_finalize   calibration.py:201-205 (finite mean in fp64, sentinel
  *                         rules, float32 cast).
+ *   bsfa_calib_select     calibration.py:126-153 thresholds_from_maxima /
+ *                         _tie_count over an explicit tile-maxima grid (the
+ *                         torch.ops.bsfa.calib_select operator).
  */
 #ifndef BSFA_B200_H
 #define BSFA_B200_H
@@ -33,7 +36,7 @@
 extern "C" {
 #endif
 
-#define BSFA_ABI_VERSION 4
+#define BSFA_ABI_VERSION 5
 
 /* error codes */
 #define BSFA_OK 0
@@ -129,6 +132,15 @@ int bsfa_debug_trace(long long* dev_buf, int cta);
 int bsfa_calib_blockmax(const bsfa_calib_args* args, void* stream);
 int bsfa_calib_finalize(const double* finite_sum, const int32_t* finite_cnt, const int32_t* neg_cnt,
                         const int32_t* pos_cnt, float* values, int64_t count, void* stream);
+/* Per (row, query position p) of a tile-maxima grid bm fp32 [rows][m_q][m_kv]
+   (scaled units, e.g. the block_maxima of bsfa_calib_blockmax), take the first
+   A_p = p * b_m / b_n entries (the off-frontier causal prefix, tiling.py:63-65),
+   and for each level k write the (k+1)-th largest (+inf for k = 0, -inf when
+   A_p <= k) to thr fp32 [num_levels][rows][m_q]; ties[s] (zeroed by the
+   caller) += positions where vals[k-1] == vals[k] (calibration.py:126-153).
+   m_kv <= 4096; 1 <= num_levels <= 16. */
+int bsfa_calib_select(const float* bm, int64_t rows, int m_q, int m_kv, int b_m, int b_n, const int32_t* k_levels,
+                      int num_levels, float* thr, unsigned long long* ties, void* stream);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ from .errors import BsfaError
 LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_O_PEERS = 7
 
 BSFA_OK = 0
@@ -43,6 +43,7 @@ EXPORTED_SYMBOLS = (
     "bsfa_debug_trace",
     "bsfa_calib_blockmax",
     "bsfa_calib_finalize",
+    "bsfa_calib_select",
 )
 
 
@@ -135,6 +136,10 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.bsfa_calib_blockmax.argtypes = [ctypes.POINTER(CalibArgs), ctypes.c_void_p]
         lib.bsfa_calib_finalize.restype = ctypes.c_int
         lib.bsfa_calib_finalize.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_void_p]
+        lib.bsfa_calib_select.restype = ctypes.c_int
+        lib.bsfa_calib_select.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p]
         if lib.bsfa_abi_version() != ABI_VERSION:
             raise NativeLibraryError(
                 f"ABI mismatch: library {lib.bsfa_abi_version()} vs binding {ABI_VERSION}")

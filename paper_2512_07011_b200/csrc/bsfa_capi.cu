@@ -381,3 +381,81 @@ extern "C" int bsfa_calib_finalize(const double* finite_sum, const int32_t* fini
   if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
   return BSFA_OK;
 }
+
+// ---------------------------------------------------------------- selection (K3)
+namespace {
+// One CTA per (row, position p): bitonic sort of the A_p tile maxima (order-
+// preserving integer image, descending) in shared memory, then per level the
+// (k+1)-th largest with the reference's sentinels and tie test.
+__global__ void __launch_bounds__(256) calib_select_kernel(const float* __restrict__ bm, int m_q, int m_kv, int b_m,
+                                                           int b_n, KernelParams lv, float* __restrict__ thr,
+                                                           unsigned long long* __restrict__ ties, long long rows) {
+  __shared__ int vals[4096];
+  const long long rp = blockIdx.x;  // row * m_q + p
+  const int p = int(rp % m_q);
+  const long long row = rp / m_q;
+  const int a = (int)(((long long)p * b_m) / b_n);
+  const float* src = bm + rp * m_kv;
+  int n2 = 1;
+  while (n2 < a) n2 <<= 1;
+  for (int x = threadIdx.x; x < n2; x += blockDim.x)
+    vals[x] = x < a ? float_to_ordered(src[x]) : float_to_ordered(-INFINITY);
+  __syncthreads();
+  for (int kk = 2; kk <= n2; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int x = threadIdx.x; x < n2; x += blockDim.x) {
+        const int y = x ^ jj;
+        if (y > x) {
+          const int u = vals[x], w = vals[y];
+          const bool desc = (x & kk) == 0;
+          if (desc ? (u < w) : (u > w)) {
+            vals[x] = w;
+            vals[y] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if ((int)threadIdx.x < lv.c_num_levels) {
+    const int k = lv.c_levels[threadIdx.x];
+    float cut;
+    bool tie = false;
+    if (k == 0) {
+      cut = INFINITY;
+    } else if (a <= k) {
+      cut = -INFINITY;
+    } else {
+      cut = ordered_to_float(vals[k]);
+      tie = vals[k - 1] == vals[k];
+    }
+    thr[((long long)threadIdx.x * rows + row) * m_q + p] = cut;
+    if (tie) atomicAdd(&ties[threadIdx.x], 1ull);
+  }
+}
+}  // namespace
+
+extern "C" int bsfa_calib_select(const float* bm, int64_t rows, int m_q, int m_kv, int b_m, int b_n,
+                                 const int32_t* k_levels, int num_levels, float* thr, unsigned long long* ties,
+                                 void* stream) {
+  if (rows < 0 || m_q < 0 || m_kv < 0 || m_kv > 4096) return fail(BSFA_ERR_INVALID, "bad grid %lld x %d x %d", (long long)rows, m_q, m_kv);
+  if (b_m < 1 || b_n < 1 || (b_m % b_n && b_n % b_m)) return fail(BSFA_ERR_INVALID, "bad tiles %dx%d", b_m, b_n);
+  if (num_levels < 1 || num_levels > 16 || !k_levels) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
+  if ((long long)(m_q - 1) * b_m / b_n > m_kv) return fail(BSFA_ERR_INVALID, "grid narrower than the causal prefix");
+  if (rows * (long long)m_q == 0) return BSFA_OK;
+  if (!bm || !thr || !ties) return fail(BSFA_ERR_INVALID, "null pointer");
+  KernelParams lv;
+  memset(&lv, 0, sizeof(lv));
+  lv.c_num_levels = num_levels;
+  for (int i = 0; i < num_levels; ++i) {
+    if (k_levels[i] < 0) return fail(BSFA_ERR_INVALID, "k levels must be >= 0");
+    lv.c_levels[i] = k_levels[i];
+  }
+  const long long grid = rows * (long long)m_q;
+  if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
+  calib_select_kernel<<<(int)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(bm, m_q, m_kv, b_m, b_n, lv, thr,
+                                                                                     ties, rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "calib_select launch");
+  return BSFA_OK;
+}

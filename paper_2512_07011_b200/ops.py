@@ -12,17 +12,21 @@
   (calibration.py:93-123), -inf elsewhere -- the calibration kernel (K2).
 * ``bsfa::calib_select(bm, k_levels) -> (thr, ties)``: per (head, position)
   the (k+1)-th largest tile maximum with the reference's sentinels
-  (calibration.py:126-153): thr fp32 [S, B, Hq, M_q], ties int64 [S].
+  (calibration.py:126-153): thr fp32 [S, B, Hq, M_q], ties int64 [S] -- one
+  ``bsfa_calib_select`` launch (K3: a bitonic sort per (head, position) in
+  shared memory).
 
 The ops carry fake (meta) implementations, so they trace under
 ``torch.compile`` / ``torch.export`` without running the kernel.  Only CUDA
 kernels are registered: the dispatcher refuses CPU tensors (no fallback).
-``calib_select`` is a selection utility over ``blockmax`` output built from
-torch ops; the calibration path itself (``calibrate`` / ``Calibrator``) fuses
-maxima, selection and accumulation in one kernel.
+The calibration path itself (``calibrate`` / ``Calibrator``) fuses maxima,
+selection and accumulation in one kernel (K2); ``blockmax`` + ``calib_select``
+expose the two halves separately.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import torch
 
@@ -95,26 +99,21 @@ def calib_select(bm: Tensor, k_levels: list[int], b_m: int, b_n: int) -> tuple[T
         raise InvalidInputError(f"bm must be fp32 [B, H, M_q, M_kv], got {bm.dtype} {tuple(bm.shape)}")
     if not k_levels or any(x < 0 for x in k_levels) or any(a >= c for a, c in zip(k_levels, k_levels[1:])):
         raise ConfigurationError(f"k levels must be non-negative and strictly increasing: {list(k_levels)}")
-    m_q, m_kv = bm.shape[2], bm.shape[3]
-    # off-frontier prefix length A_p = p * b_m // b_n (tiling.py:63-65); entries past it are ignored
-    p = torch.arange(m_q, device=bm.device)
-    a_p = (p * b_m) // b_n
-    valid = torch.arange(m_kv, device=bm.device)[None, :] < a_p[:, None]
-    vals = torch.where(valid, bm, torch.full_like(bm, float("-inf")))
-    srt = torch.sort(vals, dim=-1, descending=True).values
-    thr, ties = [], []
-    for kk in k_levels:
-        if kk == 0:
-            thr.append(torch.full(bm.shape[:3], float("inf"), dtype=torch.float32, device=bm.device))
-            ties.append(torch.zeros((), dtype=torch.int64, device=bm.device))
-            continue
-        idx = min(kk, m_kv - 1)
-        cut = srt[..., idx] if kk < m_kv else torch.full(bm.shape[:3], float("-inf"), device=bm.device)
-        enough = (a_p > kk)[None, None, :]  # len(vals) > k (calibration.py:131-136)
-        thr.append(torch.where(enough, cut, torch.full_like(cut, float("-inf"))))
-        tie = enough & (srt[..., kk - 1] == srt[..., idx]) if kk < m_kv else torch.zeros_like(enough)
-        ties.append(tie.sum().to(torch.int64))
-    return torch.stack(thr), torch.stack(ties)
+    if not bm.is_cuda:
+        raise InvalidInputError("calib_select runs on CUDA tensors only (no CPU fallback)")
+    if len(k_levels) > 16:
+        raise ConfigurationError("at most 16 sparsity levels")
+    b, h, m_q, m_kv = bm.shape
+    src = bm.contiguous()
+    thr = torch.empty((len(k_levels), b, h, m_q), dtype=torch.float32, device=bm.device)
+    ties = torch.zeros(len(k_levels), dtype=torch.int64, device=bm.device)
+    levels = (ctypes.c_int32 * len(k_levels))(*[int(x) for x in k_levels])
+    with torch.cuda.device(bm.device):
+        stream = torch.cuda.current_stream(bm.device).cuda_stream
+        _lib.check(_lib.load_library().bsfa_calib_select(
+            src.data_ptr(), b * h, m_q, m_kv, b_m, b_n, levels, len(k_levels), thr.data_ptr(), ties.data_ptr(),
+            ctypes.c_void_p(stream)), "bsfa_calib_select")
+    return thr, ties
 
 
 @calib_select.register_fake

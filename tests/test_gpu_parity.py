@@ -806,3 +806,25 @@ def test_calibrator_requires_every_layer(bsfa):
         cal.finish()
     cal.add_layer(0, 1, q, k)
     assert cal.finish().values.shape == (1, 2, 2, 4)
+
+
+def test_calib_select_kernel_exact_with_ties(bsfa):
+    """K3 (torch.ops.bsfa.calib_select): the (k+1)-th largest of each position's off-frontier prefix,
+    sentinels and tie counts exactly as calibration.py:126-153 on a grid with many equal maxima."""
+    rng = np.random.default_rng(8)
+    B, H, m_q, b_m, b_n = 2, 3, 20, 128, 64
+    m_kv = m_q * b_m // b_n
+    grid = rng.integers(0, 6, size=(B, H, m_q, m_kv)).astype(np.float32) * 0.5  # heavy ties
+    bm = torch.from_numpy(grid).cuda()
+    levels = [0, 1, 3, 8, 30]
+    thr, ties = torch.ops.bsfa.calib_select(bm, levels, b_m, b_n)
+    thr = thr.cpu().numpy()
+    want_ties = [0] * len(levels)
+    for b in range(B):
+        for h in range(H):
+            for p in range(m_q):
+                desc = np.sort(grid[b, h, p, :p * b_m // b_n])[::-1]
+                for li, kk in enumerate(levels):
+                    assert thr[li, b, h, p] == np.float32(orc.cutoff(desc, kk)), (b, h, p, kk)
+                    want_ties[li] += orc.is_tie(desc, kk)
+    assert ties.cpu().tolist() == want_ties and sum(want_ties) > 0
