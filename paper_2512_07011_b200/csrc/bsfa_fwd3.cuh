@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  if (threadIdx.x == 0) trace(12, 0, 0);  // (debug builds) CTA start, after setup
 
   if (warp == C::KPROD_WARP) {
     setmaxnreg_dec<C::REG_OTHER>();
@@ -751,6 +752,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       store_o32(p, orow + c, pk);
     }
     p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
+    if (r == 0) trace(12, 1, s);  // (debug builds) tile s's epilogue stores issued
     if (bad && p.status) atomicOr(p.status, 1);
     tc_fence_before();
     named_bar_arrive(15, C::NUM_THREADS);

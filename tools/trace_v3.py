@@ -23,7 +23,7 @@ import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
 STEPS = 2048
-EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi", "Max", "Bar", "QKw", "PVv"]
+EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi", "Max", "Bar", "QKw", "PVv", "CTA"]
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
         plan = (bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, thresholds=thr, k_level=kl, device=dev)
                 if mode == "bsfa" else bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, device=dev))
         for cta in a.cta:
-            buf = torch.zeros((24, STEPS), dtype=torch.int64, device=dev)
+            buf = torch.zeros((26, STEPS), dtype=torch.int64, device=dev)
             plan.run(q, k, v)
             lib.bsfa_debug_trace(ctypes.c_void_p(buf.data_ptr()), cta)
             plan.run(q, k, v)
@@ -59,7 +59,7 @@ def main():
             out = {"mode": mode, "cta": cta, "steps": n,
                    "cycles_per_step": float((ev["Done"][1][n - 1] - ev["Done"][1][0]) / max(1, n - 1))}
             for s in range(2):
-                S, Ld, Vo, P0, Dn, QKi, PVs, PVi, Mx, Br, QKw, PVv = (ev[x][s] for x in EV)
+                S, Ld, Vo, P0, Dn, QKi, PVs, PVi, Mx, Br, QKw, PVv, _ = (ev[x][s] for x in EV)
                 o = s ^ 1
                 out[f"s{s}"] = {
                     "wait_S(Done_j-1->S_j)": float(np.median(S[1:] - Dn[:-1])),
@@ -83,6 +83,11 @@ def main():
             Ld0, Ld1 = ev["Ld"][0], ev["Ld"][1]
             out["qk1_issue_after_ld0"] = float(np.median(QK1[:n] - Ld0[:n]))
             out["qk0_issue_after_ld1(prev)"] = float(np.median(QK0[1:n] - Ld1[:n - 1]))
+            t0, e0, e1 = t[24, 0], t[25, 0], t[25, 1]
+            out["cta_prologue(start->S0(0))"] = int(ev["S"][0][0] - t0)
+            out["cta_epilogue(Done0(last)->end0)"] = int(e0 - ev["Done"][0][n - 1])
+            out["cta_total"] = int(max(e0, e1) - t0)
+            out["cta_steps_share"] = round(float(ev["Done"][0][n - 1] - ev["S"][0][0]) / max(1, int(max(e0, e1) - t0)), 3)
             print(json.dumps(out), flush=True)
             for j in (1, 2, 3, n // 2, n // 2 + 1, n // 2 + 2):
                 if j < n:
