@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--seq", type=int, default=32768)
     ap.add_argument("--samples", type=int, default=2)
     ap.add_argument("--oracle-heads", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=3, help="interleaved (dense, BSFA) timing rounds per layer")
     ap.add_argument("--traces", default=None, help="write the evaluation decisions (reference npz trace format)")
     ap.add_argument("--report", default=None, help="write a reference schema-1 run report (JSON)")
     args = ap.parse_args()
@@ -81,31 +82,44 @@ def main():
                       "tie_counts": {str(k): int(v) for k, v in thr.diagnostics.tie_counts.items()}}),
           flush=True)
 
-    # ---- 2. held-out evaluation, dense vs BSFA per layer
+    # ---- 2. held-out evaluation, dense vs BSFA per layer.  Timing: device-only
+    # launches through BsfaPlan (same kernels attention() runs), --reps rounds
+    # of (dense, BSFA) interleaved after one warm-up pair, medians per layer.
     rows = []
     eval_sample = 1000
     traces = []
+    plan_d = bsfa.BsfaPlan(1, HQ, HKV, n, D, tiles=tiles, device=dev)
     for layer in range(L):
         q, k, v = model_dump_layer(eval_sample, layer, HQ, HKV, n, D, device=dev)
         q, k, v = q[None], k[None], v[None]
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e[0].record()
         rd = bsfa.attention(q, k, v, tiles=tiles)
-        e[1].record()
         rb = bsfa.attention(q, k, v, thresholds=thr, layer=layer, k_level=k50, tiles=tiles,
                             return_trace=args.traces is not None or args.report is not None)
-        e[2].record()
+        plan_b = bsfa.BsfaPlan(1, HQ, HKV, n, D, tiles=tiles, device=dev, thresholds=thr, layer=layer,
+                               k_level=k50)
+        td, tb = [], []
+        for r in range(args.reps + 1):
+            for plan, acc in ((plan_d, td), (plan_b, tb)):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                plan.run(q, k, v)
+                e1.record()
+                torch.cuda.synchronize()
+                if r:
+                    acc.append(e0.elapsed_time(e1))
         torch.cuda.synchronize()
         c = rb.counters.cpu().numpy()
         dev_max = float((rb.o.float() - rd.o.float()).abs().max())
         if rb.decisions is not None:
             traces.extend(traces_from_decisions(rb.decisions, tiles, causal=True, layer=layer))
-        rows.append({"layer": layer, "density": float(c[1] / c[0]), "dense_ms": e[0].elapsed_time(e[1]),
-                     "bsfa_ms": e[1].elapsed_time(e[2]), "max_abs_bsfa_vs_dense": dev_max})
+        rows.append({"layer": layer, "density": float(c[1] / c[0]), "v_fetch_frac": float(c[2] / c[3]),
+                     "dense_ms": float(np.median(td)), "bsfa_ms": float(np.median(tb)),
+                     "max_abs_bsfa_vs_dense": dev_max})
     dens = np.array([r["density"] for r in rows])
     print(json.dumps({"phase": "evaluation", "k_level": k50,
                       "predicted_density": costs.predicted_density(n, tiles, k50),
                       "measured_density_mean": float(dens.mean()), "measured_density_std": float(dens.std()),
+                      "v_fetch_frac_mean": float(np.mean([r["v_fetch_frac"] for r in rows])),
                       "dense_ms_total": sum(r["dense_ms"] for r in rows),
                       "bsfa_ms_total": sum(r["bsfa_ms"] for r in rows),
                       "speedup": sum(r["dense_ms"] for r in rows) / sum(r["bsfa_ms"] for r in rows),
