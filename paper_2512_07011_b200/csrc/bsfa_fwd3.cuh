@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
             named_bar_sync(1 + s, 160);  // the tile's vote (128 softmax threads + this warp)
             const uint4 all = lds_u128(vote_sm + (s * 2 + (j & 1)) * 16);
             w = all.x | all.y | all.z | all.w;
+            if (lane == 0) trace(13, s, j);
           } else {
             const uint32_t slot_addr = dec_sm + (s * DQ + int(dn_a[s] % DQ)) * 4;
             const uint32_t tag = dn_a[s] + 1;
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
                 tma_load_4d_w(sV + slot * C::V_UNIT + c * C::V_ATOM, &tm_v, v_full + 8 * slot, c * 64,
                               j * 128 + hh * 64, g, b, kEvictLast);
               ++vcount;
+              if (lane == 0) trace(14, s, j);
             }
           }
           prev |= hb;
@@ -346,6 +348,23 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       // S is owned by one tile at a time: every QK after the first waits for
       // the previous owner's tcgen05.ld (one s_free phase per read, in order)
       uint32_t sfree_ph = 0;
+      auto do_qk = [&](int s, int j) {
+        const unsigned u0 = unsigned(j) * NCH;
+        if (s != 0 || j != 0) ++sfree_ph;
+        if (lane == 0) trace(10, s, j);
+        tc_fence_after();
+        const int last = j < ns_a[1] ? 1 : 0;  // last reader of K(j)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const unsigned u = u0 + c;
+          const int slot = int(u % KC);
+          umma_qk_chunk_w(tmem + C::S_COL, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
+                          dk0 + uint64_t((slot * C::K_CHUNK) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
+          if (s == last) umma_commit_w(k_empty + 8 * slot);
+        }
+        umma_commit_w(s_full + 8 * s);
+        if (lane == 0) trace(5, s, j);
+      };
       auto issue_qk = [&](int s, int j) {
         const unsigned u0 = unsigned(j) * NCH;
         const bool wait_s = s != 0 || j != 0;
@@ -361,22 +380,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         } else {
           mbar_wait(s_free, sfree_ph & 1u);
         }
-        if (wait_s) ++sfree_ph;
-        if (lane == 0) trace(10, s, j);
-        tc_fence_after();
-        const int last = j < ns_a[1] ? 1 : 0;  // last reader of K(j)
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          const unsigned u = u0 + c;
-          const int slot = int(u % KC);
-          umma_qk_chunk_w(tmem + C::S_COL, dq0 + uint64_t((s * C::Q_TILE + c * C::Q_ATOM) >> 4),
-                          dk0 + uint64_t((slot * C::K_CHUNK) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
-          if (s == last) umma_commit_w(k_empty + 8 * slot);
-        }
-        umma_commit_w(s_full + 8 * s);
-        if (lane == 0) trace(5, s, j);
+        do_qk(s, j);
       };
-
       unsigned vbase = 0;      // V units consumed before this step
       unsigned nunits = 0;     // V units of the current step
       uint32_t prev = 0;       // 64-key halves of the current step already given a unit
@@ -384,9 +389,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       uint32_t o_started = 0;  // bit s: O_s holds a partial sum
       unsigned dn_m[2] = {0u, 0u};                // voted decisions read, per tile
       unsigned long long kept_m = 0;              // processed gate tiles (counters[1])
-      auto issue_pv = [&](int s, int j) {
-        const int sb = sbits(j, qi_a[s]);
-        mbar_wait(p_full + 16 * s + 8 * (j & 1), (j >> 1) & 1);
+      // PV_s(j), part 1 (after p_full): the tile's decision -> 64-key halves kept
+      // and their V unit numbers (units numbered in the producer's fetch order)
+      auto pv_decide = [&](int s, int j) -> uint32_t {
+        const int sb = sbits(j, s ? qi_a[1] : qi_a[0]);  // (selects: s may be a runtime value)
         tc_fence_after();
         if (lane == 0) trace(6, s, j);
         uint32_t bits;
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           bits = uint32_t(sb);
         } else if constexpr (VP) {
           // the vote words of step j: rewritten only at step j + 2, whose vote
-          // needs QK_s(j+2), issued after this PV
+          // needs QK_s(j+2), issued after this decision is read
           const uint4 all = lds_u128(vote_sm + (s * 2 + (j & 1)) * 16);
           bits = all.x | all.y | all.z | all.w;
         } else {
@@ -410,6 +416,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         for (int hh = 0; hh < 2; ++hh)
           if (((hb & ~prev) >> hh) & 1u) uidx[hh] = vbase + nunits++;
         prev |= hb;
+        return hb;
+      };
+      // part 2: per kept half, wait for its V unit and issue its MMAs; commits
+      auto pv_mma = [&](int s, int j, uint32_t hb) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           if ((hb >> hh) & 1u) {
@@ -429,8 +439,18 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         // phase per step that issued PVs, each with a waiter (compute-sanitizer
         // synccheck reports skipped phases as "missing wait").
         if (!BSFA_PV_EVERY_PHASE || hb) umma_commit_w(pv_done + 8 * s);
-        if (j == ns_a[s] - 1) umma_commit_w(o_full + 8 * s);
+        if (j == (s ? ns_a[1] : ns_a[0]) - 1) umma_commit_w(o_full + 8 * s);
         if (lane == 0) trace(7, s, j);
+      };
+      auto issue_pv = [&](int s, int j) {
+        mbar_wait(p_full + 16 * s + 8 * (j & 1), (j >> 1) & 1);
+        pv_mma(s, j, pv_decide(s, j));
+      };
+      auto end_pv_step = [&]() {
+        for (unsigned x = 0; x < nunits; ++x) umma_commit_w(v_empty + 8 * ((vbase + x) % VS));
+        vbase += nunits;
+        prev = 0;
+        nunits = 0;
       };
 
       if (qk_role) {
@@ -438,16 +458,11 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         if (ns_a[1] > 0) issue_qk(1, 0);
       }
       for (int j = 0; j < nsteps; ++j) {
-        prev = 0;
-        nunits = 0;
         if (qk_role && j + 1 < ns_a[0]) issue_qk(0, j + 1);
         if (pv_role) issue_pv(0, j);
         if (qk_role && j + 1 < ns_a[1]) issue_qk(1, j + 1);
         if (pv_role && j < ns_a[1]) issue_pv(1, j);
-        if (pv_role) {
-          for (unsigned x = 0; x < nunits; ++x) umma_commit_w(v_empty + 8 * ((vbase + x) % VS));
-          vbase += nunits;
-        }
+        if (pv_role) end_pv_step();
       }
       if (pv_role && lane == 0 && p.counters) {
         atomicAdd(&p.counters[0], (unsigned long long)(ns_a[0] + ns_a[1]) * GT);

@@ -23,7 +23,7 @@ import paper_2512_07011_b200 as bsfa  # noqa: E402
 from paper_2512_07011_b200 import _lib, costs  # noqa: E402
 
 STEPS = 2048
-EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi", "Max", "Bar", "QKw", "PVv", "CTA"]
+EV = ["S", "Ld", "Vote", "P0", "Done", "QKi", "PVseen", "PVi", "Max", "Bar", "QKw", "PVv", "CTA", "Vvote", "Vtma"]
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
         plan = (bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, thresholds=thr, k_level=kl, device=dev)
                 if mode == "bsfa" else bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, device=dev))
         for cta in a.cta:
-            buf = torch.zeros((26, STEPS), dtype=torch.int64, device=dev)
+            buf = torch.zeros((30, STEPS), dtype=torch.int64, device=dev)
             plan.run(q, k, v)
             lib.bsfa_debug_trace(ctypes.c_void_p(buf.data_ptr()), cta)
             plan.run(q, k, v)
@@ -59,7 +59,7 @@ def main():
             out = {"mode": mode, "cta": cta, "steps": n,
                    "cycles_per_step": float((ev["Done"][1][n - 1] - ev["Done"][1][0]) / max(1, n - 1))}
             for s in range(2):
-                S, Ld, Vo, P0, Dn, QKi, PVs, PVi, Mx, Br, QKw, PVv, _ = (ev[x][s] for x in EV)
+                S, Ld, Vo, P0, Dn, QKi, PVs, PVi, Mx, Br, QKw, PVv, _, Vv, Vt = (ev[x][s] for x in EV)
                 o = s ^ 1
                 out[f"s{s}"] = {
                     "wait_S(Done_j-1->S_j)": float(np.median(S[1:] - Dn[:-1])),
@@ -77,6 +77,9 @@ def main():
                     "  qk_mma_issue(QKw->QKi)": float(np.median(QKi - QKw)),
                     "  pv_vwait(PVseen->PVv, kept)": float(np.median((PVv - PVs)[PVv > PVs])) if (PVv > PVs).any() else -1,
                     "  pv_mma_issue(PVv->PVi, kept)": float(np.median((PVi - PVv)[PVv > PVs])) if (PVv > PVs).any() else -1,
+                    "vprod_vote_seen(Vote->Vvote)": float(np.median(Vv - Vo)),
+                    "vprod_tma(Vvote->Vtma, issued)": float(np.median((Vt - Vv)[Vt > Vv])) if (Vt > Vv).any() else -1,
+                    "v_latency(Vtma->PVv, kept)": float(np.median((PVv - Vt)[(PVv > PVs) & (Vt > Vv)])) if ((PVv > PVs) & (Vt > Vv)).any() else -1,
                 }
             # QK issue lag behind the previous S owner's release
             QK0, QK1 = ev["QKi"][0], ev["QKi"][1]
