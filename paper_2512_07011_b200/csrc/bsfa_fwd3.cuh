@@ -71,6 +71,14 @@
 #ifndef BSFA_FWD3_SPLIT
 #define BSFA_FWD3_SPLIT 0
 #endif
+// S release (softmax -> MMA warp) through a named barrier (bar.arrive by the
+// tile's 128 threads, bar.sync by the issuer) instead of an mbarrier phase:
+// 0 never, 1 always, 2 for the statically gated kernels (GM == 1: dense,
+// frontier-only, sliding window), where it measured 2-4 % faster; the voted
+// kernels measured 4-6 % slower with it
+#ifndef BSFA_SFREE_NB
+#define BSFA_SFREE_NB 2
+#endif
 
 namespace bsfa {
 
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   // statically known decision bits of step j for query block qi (-1: voted)
   // the V producer reads ThresholdGate decisions straight from the vote words
   constexpr bool VP = GM == 0 && GT == 2 && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
+  constexpr bool SNB = !BSFA_FWD3_SPLIT && (BSFA_SFREE_NB == 1 || (BSFA_SFREE_NB == 2 && GM == 1));
   auto sbits = [&](int j, int qi) -> int {
     if constexpr (GM == 1) return step_static_bits<GT>(gate_mode, window, j, qi);
     return j == qi ? (1 << GT) - 1 : -1;  // frontier (tiling.py:50-60)
@@ -368,7 +377,12 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       auto issue_qk = [&](int s, int j) {
         const unsigned u0 = unsigned(j) * NCH;
         const bool wait_s = s != 0 || j != 0;
-        if (s == 0) {
+        if (SNB) {
+          // K(j) first (tile 0 is its first reader), then the S release
+          if (s == 0)
+            for (int c = 0; c < NCH; ++c) mbar_wait(k_full + 8 * int((u0 + c) % KC), ((u0 + c) / KC) & 1);
+          if (wait_s) named_bar_sync(5, 160);
+        } else if (s == 0) {
           // tile 0 is the first reader of K(j): S free + every chunk landed, tested together
           if (NCH == 2 && wait_s)
             mbar_wait3(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1,
@@ -535,8 +549,14 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
       tmem_wait_ld();
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);  // the other tile's QK may overwrite S
+      if (SNB) {
+        // the other tile's QK may overwrite S; no arrival after the CTA's last
+        // S read (a named barrier has no phases to leave behind)
+        if (s == 0 ? (j < ns_a[1] || j + 1 < ns_a[0]) : j + 1 < ns_a[0]) named_bar_arrive(5, 160);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);  // the other tile's QK may overwrite S
+      }
       if (r == 0) trace(1, s, j);
 
       const int sb = sbits(j, qi_s);
