@@ -9,7 +9,19 @@
 
 #include "../../include/bsfa_b200.h"
 #include "bsfa_calib.cuh"    // K2: calibration block maxima + cutoffs
-#include "bsfa_fwd3.cuh"     // K1: forward (shared S, P in TMEM)
+#include "bsfa_fwd3.cuh"     // K1: forward (two query tiles per CTA, one shared S, P in TMEM)
+#define BSFA_FWD_KERNEL bsfa_fwd3_kernel
+#define BSFA_FWD_CFG FCfg3
+// Measurement builds only (-DBSFA_FWD_PAIR=1, tools/build_variants.sh): head_dim
+// 128 with an even GQA group on CTA pairs, experimental/csrc/bsfa_fwd7.cuh
+// (measured 45 % slower); the production library does
+// not contain it.
+#ifndef BSFA_FWD_PAIR
+#define BSFA_FWD_PAIR 0
+#endif
+#if BSFA_FWD_PAIR
+#include "../../experimental/csrc/bsfa_fwd7.cuh"
+#endif
 // The round-1 forward and the other measured alternatives live in
 // experimental/csrc (not built); DESIGN.md section 5 has their numbers.
 
@@ -111,16 +123,16 @@ int launch_calib(const CUtensorMap& tq, const CUtensorMap& tk, const KernelParam
 template <int D, int GT>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
                cudaStream_t st) {
-  using C = FCfg3<D, GT>;
-  // gate class and causality are template parameters of the v3 kernel
+  using C = BSFA_FWD_CFG<D, GT>;
+  // gate class and causality are template parameters of the forward kernel
   const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) = nullptr;
   int rc = BSFA_OK;
   const int smem = C::SMEM_BYTES;
 #define BSFA_GM(GM_, CA_)                                                                     \
   if (gm == GM_ && (p.causal != 0) == CA_) {                                                  \
-    kern = bsfa_fwd3_kernel<D, GT, GM_, CA_>;                                                 \
-    rc = ensure_smem_attr<bsfa_fwd3_kernel<D, GT, GM_, CA_>>(C::SMEM_BYTES);                  \
+    kern = BSFA_FWD_KERNEL<D, GT, GM_, CA_>;                                                  \
+    rc = ensure_smem_attr<BSFA_FWD_KERNEL<D, GT, GM_, CA_>>(C::SMEM_BYTES);                   \
   }
   BSFA_GM(0, true)
   BSFA_GM(0, false)
@@ -136,6 +148,37 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   if (e != cudaSuccess) return cuda_fail(e, "bsfa forward launch");
   return BSFA_OK;
 }
+
+#if BSFA_FWD_PAIR
+// forward K1 on CTA pairs (bsfa_fwd7.cuh): clusters of two, grid = 2 x units
+template <int GT>
+int launch_fwd7(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+                cudaStream_t st) {
+  using C = FCfg7<GT>;
+  const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) = nullptr;
+  int rc = BSFA_OK;
+#define BSFA_GM7(GM_, CA_)                                                  \
+  if (gm == GM_ && (p.causal != 0) == CA_) {                               \
+    kern = bsfa_fwd7_kernel<GT, GM_, CA_>;                                 \
+    rc = ensure_smem_attr<bsfa_fwd7_kernel<GT, GM_, CA_>>(C::SMEM_BYTES);  \
+  }
+  BSFA_GM7(0, true)
+  BSFA_GM7(0, false)
+  BSFA_GM7(1, true)
+  BSFA_GM7(1, false)
+  BSFA_GM7(2, true)
+  BSFA_GM7(2, false)
+#undef BSFA_GM7
+  if (rc) return rc;
+  if (grid == 0) return BSFA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa forward (CTA pair) launch");
+  return BSFA_OK;
+}
+
+#endif
 
 int dispatch_fwd(int d, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                  const KernelParams& p, int grid, cudaStream_t st) {
@@ -223,8 +266,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   CUtensorMap tq, tk, tv;
   if (int rc = make_map(&tq, a->q, d, n, a->heads_q, a->batch, a->q_stride_n, a->q_stride_h, a->q_stride_b, 128, "q"))
     return rc;
+  // (measurement builds) CTA pairs, d = 128, even GQA group: each CTA stages 64 keys of a step
+  const bool pair = BSFA_FWD_PAIR && d == 128 && (a->heads_q / a->heads_kv) % 2 == 0;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
-128, "k"))
+                        pair ? 64 : 128, "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b,
@@ -279,6 +324,13 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
   (void)nq;
+#if BSFA_FWD_PAIR
+  if (pair) {
+    if (2 * grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
+    if (a->b_n == 64) return launch_fwd7<2>(tq, tk, tv, p, (int)(2 * grid), reinterpret_cast<cudaStream_t>(stream));
+    return launch_fwd7<1>(tq, tk, tv, p, (int)(2 * grid), reinterpret_cast<cudaStream_t>(stream));
+  }
+#endif
   return dispatch_fwd(d, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 

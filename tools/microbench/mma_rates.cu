@@ -29,7 +29,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
 __global__ void __launch_bounds__(128, 1) k(long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 131072);
+  const uint32_t bar = smem_u32(base + 131072);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(base + 131072 + 64);
   for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x3c003c00u;
   const int warp = threadIdx.x >> 5;
