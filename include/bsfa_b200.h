@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define BSFA_ABI_VERSION 5
+#define BSFA_ABI_VERSION 6
 
 /* error codes */
 #define BSFA_OK 0
@@ -74,6 +74,9 @@ typedef struct bsfa_fwd_args {
   int64_t o_stride_b, o_stride_h, o_stride_n;
   float* lse;        /* fp32 [batch][heads_q][seq_len], natural log, scaled-score units */
   int8_t* decisions; /* optional int8 [batch][heads_q][seq_len/b_m][seq_len/b_n]; caller zeroes */
+  /* tiles: b_m in {64, 128}, b_n in {64, 128}; seq_len a multiple of 128 (pad
+     by repeating the last row); valid_len = unpadded length.  With b_m = 64 the
+     counters count only the reference grid padded to lcm(b_m, b_n). */
   unsigned long long* counters; /* optional [4], see BSFA_CNT_* */
   int* status; /* optional; bit 0 set if any row has a non-finite accumulator or l <= 0 */
   /* gate */
@@ -116,6 +119,10 @@ typedef struct bsfa_calib_args {
   /* optional raw tile maxima fp32 [heads_q][seq_len/b_m][seq_len/b_n] (unsorted,
      scaled units); entries outside the off-frontier prefix are left untouched */
   float* block_maxima;
+  /* the sample's padded length in the reference grid (a multiple of b_m and b_n,
+     <= seq_len; 0 = seq_len): query blocks past it (seq_len is padded further
+     to a multiple of 128 for the kernel) contribute nothing.  ABI 6. */
+  int valid_len;
 } bsfa_calib_args;
 
 int bsfa_abi_version(void);

@@ -10,7 +10,7 @@ batched GQA entry point on CUDA tensors.
 
 from .errors import (BsfaError, ConfigurationError, DegenerateRowError, FormatError,
                      InvalidInputError, NumericError)
-from .tiling import (TileConfig, frontier_blocks, frontier_count, kernel_supports,
+from .tiling import (TileConfig, frontier_blocks, frontier_count, kernel_len, kernel_supports,
                      off_frontier_count)
 from .thresholds import ThresholdTensor, load_thresholds, save_thresholds, threshold_lookup
 from .gates import (DenseGate, FrontierOnlyGate, GateContext, RunningMaxGate, SlidingWindowGate,

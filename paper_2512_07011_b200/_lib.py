@@ -16,7 +16,7 @@ from .errors import BsfaError
 LIB_PATH = os.environ.get("BSFA_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libbsfa_b200.so")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 MAX_O_PEERS = 7
 
 BSFA_OK = 0
@@ -100,6 +100,7 @@ class CalibArgs(ctypes.Structure):
         ("pos_cnt", ctypes.c_void_p),
         ("tie_counts", ctypes.c_void_p),
         ("block_maxima", ctypes.c_void_p),
+        ("valid_len", ctypes.c_int),
     ]
 
 

@@ -39,7 +39,7 @@ from .core import AttentionOutput, HeadInput
 from .errors import ConfigurationError, InvalidInputError, NumericError
 from .gates import GateContext, ThresholdGate, gate_params, kernel_gate_mode
 from .thresholds import ThresholdTensor
-from .tiling import TileConfig, require_kernel_tiles
+from .tiling import TileConfig, kernel_len, require_kernel_tiles
 from .trace import GateTrace
 
 
@@ -151,7 +151,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool
     zero normaliser.  Pass ``False`` in stream-ordered serving loops (or use
     :class:`BsfaPlan`) and inspect ``result.status`` when convenient.
 
-    ``out`` (bf16 [B, Hq, n_pad, d_pad], unit head_dim stride, 16-byte aligned
+    ``out`` (bf16 [B, Hq, n_kern, d_pad], n_kern = ``tiling.kernel_len(n, tiles)``, unit head_dim stride, 16-byte aligned
     rows) receives O instead of a fresh tensor; ``o_peers`` are device
     addresses of further copies with ``out``'s strides (peer GPUs' slots of a
     gathered-O buffer mapped over NVLink) that the kernel epilogue writes
@@ -193,31 +193,32 @@ def _forward(q, k, v, thr_dev, mode: int, window: int, lam: float, *, causal: bo
     bsz, hq, n, d = q.shape
     hkv = k.shape[1]
     thr_positions = int(thr_dev.shape[1]) if thr_dev is not None else 0
-    n_pad = tiles.padded_len(n)
+    n_pad = tiles.padded_len(n)  # the reference grid
+    n_kern = kernel_len(n, tiles)  # n_pad rounded up to the kernels' 128 rows
     d_pad = 64 if d <= 64 else 128
     sc = reference_scale(d) if scale is None else float(np.float32(scale))
 
     dev = q.device
     with torch.cuda.device(dev):
-        qk = _as_kernel_operand(q, n_pad, d_pad)
-        kk = _as_kernel_operand(k, n_pad, d_pad)
-        vk = _as_kernel_operand(v, n_pad, d_pad)
+        qk = _as_kernel_operand(q, n_kern, d_pad)
+        kk = _as_kernel_operand(k, n_kern, d_pad)
+        vk = _as_kernel_operand(v, n_kern, d_pad)
         o_peers = [int(x) for x in o_peers]
         if out is not None:
-            if (tuple(out.shape) != (bsz, hq, n_pad, d_pad) or out.dtype != torch.bfloat16 or out.device != dev
+            if (tuple(out.shape) != (bsz, hq, n_kern, d_pad) or out.dtype != torch.bfloat16 or out.device != dev
                     or out.stride(3) != 1 or (out.stride(2) * 2) % 16 or out.data_ptr() % 16):
                 raise InvalidInputError(
-                    f"out must be bf16 {(bsz, hq, n_pad, d_pad)} on {dev} with unit head_dim stride and "
+                    f"out must be bf16 {(bsz, hq, n_kern, d_pad)} on {dev} with unit head_dim stride and "
                     "16-byte aligned rows")
             o = out
         elif o_peers:
             raise InvalidInputError("o_peers mirror out's layout: pass out as well")
         else:
-            o = torch.empty((bsz, hq, n_pad, d_pad), dtype=torch.bfloat16, device=dev)
+            o = torch.empty((bsz, hq, n_kern, d_pad), dtype=torch.bfloat16, device=dev)
         if len(o_peers) > _lib.MAX_O_PEERS:
             raise ConfigurationError(f"at most {_lib.MAX_O_PEERS} peer copies of O")
-        lse = torch.empty((bsz, hq, n_pad), dtype=torch.float32, device=dev)
-        m_q, m_kv = n_pad // tiles.b_m, n_pad // tiles.b_n
+        lse = torch.empty((bsz, hq, n_kern), dtype=torch.float32, device=dev)
+        m_q, m_kv = n_kern // tiles.b_m, n_kern // tiles.b_n
         dec = torch.zeros((bsz, hq, m_q, m_kv), dtype=torch.int8, device=dev) if return_trace else None
         counters = torch.zeros(4, dtype=torch.int64, device=dev)
         status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -237,7 +238,7 @@ def _forward(q, k, v, thr_dev, mode: int, window: int, lam: float, *, causal: bo
         a.thr_positions = thr_positions
         a.gate_mode = mode
         a.batch, a.heads_q, a.heads_kv = bsz, hq, hkv
-        a.seq_len, a.valid_len, a.head_dim = n_pad, n, d_pad
+        a.seq_len, a.valid_len, a.head_dim = n_kern, n, d_pad
         a.b_m, a.b_n = tiles.b_m, tiles.b_n
         a.causal = 1 if causal else 0
         a.scale = sc
@@ -249,9 +250,11 @@ def _forward(q, k, v, thr_dev, mode: int, window: int, lam: float, *, causal: bo
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(_lib.load_library().bsfa_fwd(ctypes.byref(a), ctypes.c_void_p(stream)), "bsfa_fwd")
 
-    if n_pad != n or d_pad != d:
+    if n_kern != n or d_pad != d:
         o = o[:, :, :n, :d]
         lse = lse[:, :, :n]
+    if dec is not None and n_kern != n_pad:  # the reference grid (b_m = 64, odd block count)
+        dec = dec[:, :, :n_pad // tiles.b_m, :n_pad // tiles.b_n]
     return AttentionResult(o=o, lse=lse, decisions=dec, counters=counters, status=status)
 
 
@@ -321,7 +324,7 @@ class BsfaPlan:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.tiles = tiles
         self.n = seq_len
-        self.n_pad = tiles.padded_len(seq_len)
+        self.n_pad = kernel_len(seq_len, tiles)  # the reference padding rounded up to 128 rows
         self.shape_q = (batch, heads_q, self.n_pad, head_dim)
         self.shape_kv = (batch, heads_kv, self.n_pad, head_dim)
         dev = self.device

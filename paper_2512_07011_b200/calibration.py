@@ -27,7 +27,7 @@ from . import _lib
 from .attention import reference_scale
 from .errors import ConfigurationError, InvalidInputError
 from .thresholds import ThresholdTensor
-from .tiling import TileConfig, off_frontier_count, require_kernel_tiles
+from .tiling import TileConfig, kernel_len, off_frontier_count, require_kernel_tiles
 
 
 def _to_array(x):
@@ -164,7 +164,11 @@ class Calibrator:
 
     def add_layer(self, sample_id: int, layer: int, q, k, seq_len: int | None = None,
                   block_maxima: torch.Tensor | None = None) -> None:
-        """q [Hq, N, d], k [Hkv, N, d] of one (sample, layer); any float dtype/device."""
+        """q [Hq, N, d], k [Hkv, N, d] of one (sample, layer); any float dtype/device.
+
+        ``block_maxima`` (optional) receives the raw tile maxima on the kernel
+        grid, fp32 [Hq, n_kern / b_m, n_kern / b_n], n_kern = kernel_len(N).
+        """
         key = (int(sample_id), int(layer))
         if self._last is not None and key[0] < self._last[0]:
             raise ConfigurationError("samples must be added in non-decreasing sample-id order")
@@ -172,12 +176,13 @@ class Calibrator:
         if not self.sample_ids or self.sample_ids[-1] != key[0]:
             self.sample_ids.append(key[0])
         n = int(q.shape[1]) if seq_len is None else int(seq_len)
-        n_pad = self.tiles.padded_len(n)
+        n_pad = self.tiles.padded_len(n)   # the reference grid of this sample
+        n_kern = kernel_len(n, self.tiles)  # rounded up to the kernel's 128 rows
         if n_pad > self.n_max:
             raise ConfigurationError(f"sample length {n} exceeds calibrator n_max {self.n_max}")
         d_pad = 64 if self.head_dim <= 64 else 128
-        qd = _head_operand(q, n_pad, d_pad, self.device)
-        kd = _head_operand(k, n_pad, d_pad, self.device)
+        qd = _head_operand(q, n_kern, d_pad, self.device)
+        kd = _head_operand(k, n_kern, d_pad, self.device)
         if qd.shape[0] != self.num_heads:
             raise ConfigurationError(f"layer has {qd.shape[0]} q heads, calibrator expects {self.num_heads}")
         self.nonfinite |= ~(torch.isfinite(qd).all() & torch.isfinite(kd).all())
@@ -188,7 +193,8 @@ class Calibrator:
         a.q, a.k = qd.data_ptr(), kd.data_ptr()
         a.q_stride_h, a.q_stride_n = qd.stride(0), qd.stride(1)
         a.k_stride_h, a.k_stride_n = kd.stride(0), kd.stride(1)
-        a.heads_q, a.heads_kv, a.seq_len, a.head_dim = qd.shape[0], kd.shape[0], n_pad, d_pad
+        a.heads_q, a.heads_kv, a.seq_len, a.head_dim = qd.shape[0], kd.shape[0], n_kern, d_pad
+        a.valid_len = n_pad
         a.b_m, a.b_n = self.tiles.b_m, self.tiles.b_n
         a.scale = reference_scale(self.head_dim)
         a.layer, a.num_layers, a.num_positions = layer, self.num_layers, self.num_positions
@@ -258,13 +264,14 @@ def collect_block_maxima(sample: CalibrationSample, tiles: TileConfig, device=No
     """Sorted off-frontier tile maxima per (layer, head, position) (calibration.py:93-123)."""
     require_kernel_tiles(tiles)
     n_pad = tiles.padded_len(sample.seq_len)
+    n_kern = kernel_len(sample.seq_len, tiles)
     L, H, _, d = sample.q.shape
     num_p = n_pad // tiles.b_m
-    m_kv = n_pad // tiles.b_n
     cal = Calibrator([0], tiles, L, H, n_pad, d, device=device)
     maxima = {}
     for layer in range(L):
-        bm = torch.full((H, num_p, m_kv), float("nan"), dtype=torch.float32, device=cal.device)
+        bm = torch.full((H, n_kern // tiles.b_m, n_kern // tiles.b_n), float("nan"), dtype=torch.float32,
+                        device=cal.device)
         cal.add_layer(sample.sample_id, layer, sample.q[layer], sample.k[layer], seq_len=sample.seq_len,
                       block_maxima=bm)
         bm_sorted = torch.sort(torch.nan_to_num(bm, nan=-float("inf")), dim=2, descending=True).values.cpu().numpy()

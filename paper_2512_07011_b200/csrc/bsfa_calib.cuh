@@ -26,17 +26,18 @@
 
 namespace bsfa {
 
-template <int D, int GT>
+template <int D, int GT, int BM = 128>
 struct CCfg {
   static constexpr int NCH = D / 64;           // 64-column swizzle atoms along head_dim
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = 128 * D * 2;   // one 128-key step
   static constexpr int KS = 3;                 // K ring stages
   static constexpr int MAXA = 4096;            // max off-frontier gate tiles per row
+  static constexpr int NBLK = 128 / BM;        // query blocks per 128-row tile
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
-  static constexpr int OFF_CAL = OFF_K + KS * K_TILE;      // int [2][MAXA] ordered maxima
-  static constexpr int OFF_BAR = OFF_CAL + 2 * MAXA * 4;
+  static constexpr int OFF_CAL = OFF_K + KS * K_TILE;      // int [2 tiles][NBLK][MAXA] ordered maxima
+  static constexpr int OFF_BAR = OFF_CAL + 2 * NBLK * MAXA * 4;
   // bar_q, k_full/empty[KS], s_full[2][2 buffers], s_read[2][2 buffers]
   static constexpr int NUM_BARS = 1 + 2 * KS + 4 + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
@@ -48,15 +49,19 @@ struct CCfg {
   static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8;
   static constexpr int REG_SOFT = (NUM_THREADS * REG_LAUNCH - 128 * REG_OTHER) / 256 / 8 * 8;
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
+  static_assert(BM == 128 || BM == 64, "b_m in {64, 128}");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-template <int D, int GT>
-__global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
+// BM = 64: a 128-row tile holds query blocks 2t (rows 0-63) and 2t+1 (rows
+// 64-127); each block has its own off-frontier prefix A = blk * 64 / b_n, its
+// own maxima row (warps 0-1 / 2-3 of the tile) and its own cutoffs.
+template <int D, int GT, int BM = 128>
+__global__ void __launch_bounds__(CCfg<D, GT, BM>::NUM_THREADS, 1)
     bsfa_calib_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const KernelParams p) {
-  using C = CCfg<D, GT>;
-  constexpr int KS = C::KS, NCH = C::NCH;
+  using C = CCfg<D, GT, BM>;
+  constexpr int KS = C::KS, NCH = C::NCH, NBLK = C::NBLK;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
@@ -102,9 +107,13 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
     }
   }
   const int g = g_;
-  // the off-frontier causal prefix j < i (calibration.py:110-113)
+  // the off-frontier causal prefix (calibration.py:110-113): j < i for b_m =
+  // 128; for b_m = 64 the 128-key steps holding the prefix of block 2t+1
+  constexpr int BN = 128 / GT;
+  auto a_of = [](int blk) { return blk * BM / BN; };  // A_blk, tiling.py:63-65
 #pragma unroll
-  for (int t = 0; t < 2; ++t) ns_a[t] = qi_a[t] < 0 ? 0 : qi_a[t];
+  for (int t = 0; t < 2; ++t)
+    ns_a[t] = qi_a[t] < 0 ? 0 : (BM == 128 ? qi_a[t] : (a_of(2 * qi_a[t] + 1) + GT - 1) / GT);
   const int nsteps = ns_a[0];
 
   // ---- setup
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
     }
     fence_mbarrier_init();
   }
-  for (int i = threadIdx.x; i < 2 * C::MAXA; i += blockDim.x) cvals[i] = float_to_ordered(-INFINITY);
+  for (int i = threadIdx.x; i < 2 * NBLK * C::MAXA; i += blockDim.x) cvals[i] = float_to_ordered(-INFINITY);
   if (warp == C::MMA_WARP) {
     tmem_alloc(tmem_ptr, C::TMEM_COLS);
     tmem_relinquish();
@@ -210,7 +219,10 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
     }
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const float scale = p.scale;
-    int* vals = cvals + s * C::MAXA;
+    const int hf = BM == 64 ? (r >> 6) : 0;          // this thread's query block in the tile
+    const int blk = BM == 64 ? 2 * qi_s + hf : qi_s;
+    const int A = BM == 64 ? a_of(blk) : nst * GT;   // this block's off-frontier prefix (gate tiles)
+    int* vals = cvals + (s * NBLK + hf) * C::MAXA;
     for (int j = 0; j < nst; ++j) {
       const int buf = 2 * s + (j & 1);
       mbar_wait(s_full + 8 * buf, (j >> 1) & 1);
@@ -255,22 +267,28 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
 #pragma unroll
       for (int x = 0; x < GT; ++x) {
         const int m = __reduce_max_sync(0xffffffffu, float_to_ordered(mx[x] * scale));
-        if (lane == 0) atomicMax(&vals[j * GT + x], m);
+        if (lane == 0 && (BM == 128 || j * GT + x < A)) atomicMax(&vals[j * GT + x], m);
       }
     }
 
     // ---- order statistics of this row of gate-tile maxima (calibration.py:116-153)
-    const int A = nst * GT;
-    named_bar_sync(3 + s, 128);
-    if (p.c_maxima) {
-      float* out = p.c_maxima + ((long long)hq * p.num_q_tiles + qi_s) * p.gate_cols;
-      for (int x = r; x < A; x += 128) out[x] = ordered_to_float(vals[x]);
+    // (b_m = 64: each block sorts its own row with its 64 threads)
+    constexpr int NT = BM;  // threads per query block
+    const int rt = BM == 64 ? (r & 63) : r;
+    const int bar_id = BM == 64 ? 6 + 2 * s + hf : 3 + s;
+    // query blocks past the sample's reference grid (the kernel pads to 128 rows) add nothing
+    const int blk_valid = p.valid_len / BM;  // valid_len = the sample's padded length (a multiple of lcm(b_m, b_n))
+    const bool live = blk < blk_valid;
+    named_bar_sync(bar_id, NT);
+    if (p.c_maxima && live) {
+      float* out = p.c_maxima + ((long long)hq * (p.num_q_tiles * NBLK) + blk) * p.gate_cols;
+      for (int x = rt; x < A; x += NT) out[x] = ordered_to_float(vals[x]);
     }
     int n2 = 1;
     while (n2 < A) n2 <<= 1;
     for (int kk = 2; kk <= n2; kk <<= 1) {
       for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        for (int x = r; x < n2; x += 128) {
+        for (int x = rt; x < n2; x += NT) {
           const int y = x ^ jj;
           if (y > x) {
             const int a = vals[x], c = vals[y];
@@ -281,11 +299,11 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
             }
           }
         }
-        named_bar_sync(3 + s, 128);
+        named_bar_sync(bar_id, NT);
       }
     }
-    if (r < p.c_num_levels) {
-      const int k = p.c_levels[r];
+    if (live && rt < p.c_num_levels) {
+      const int k = p.c_levels[rt];
       float cut;
       bool tie = false;
       if (k == 0) {
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
         cut = ordered_to_float(vals[k]);
         tie = vals[k - 1] == vals[k];
       }
-      const long long idx = (((long long)r * p.c_num_layers + p.c_layer) * p.heads_q + hq) * p.c_positions + qi_s;
+      const long long idx = (((long long)rt * p.c_num_layers + p.c_layer) * p.heads_q + hq) * p.c_positions + blk;
       if (isfinite(cut)) {
         p.c_sum[idx] += (double)cut;
         p.c_fin[idx] += 1;
@@ -305,7 +323,7 @@ __global__ void __launch_bounds__(CCfg<D, GT>::NUM_THREADS, 1)
       } else {
         p.c_pos[idx] += 1;
       }
-      if (tie) atomicAdd(&p.c_ties[r], 1ull);
+      if (tie) atomicAdd(&p.c_ties[rt], 1ull);
     }
     named_bar_arrive(15, C::NUM_THREADS);
     return;

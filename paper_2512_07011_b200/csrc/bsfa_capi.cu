@@ -107,11 +107,11 @@ int ensure_smem_attr(int bytes) {
 }
 
 // calibration kernel K2 (bsfa_calib.cuh)
-template <int D, int GT>
+template <int D, int GT, int BM>
 int launch_calib(const CUtensorMap& tq, const CUtensorMap& tk, const KernelParams& p, int grid, cudaStream_t st) {
-  using C = CCfg<D, GT>;
-  auto kern = bsfa_calib_kernel<D, GT>;
-  if (int rc = ensure_smem_attr<bsfa_calib_kernel<D, GT>>(C::SMEM_BYTES)) return rc;
+  using C = CCfg<D, GT, BM>;
+  auto kern = bsfa_calib_kernel<D, GT, BM>;
+  if (int rc = ensure_smem_attr<bsfa_calib_kernel<D, GT, BM>>(C::SMEM_BYTES)) return rc;
   if (grid == 0) return BSFA_OK;
   kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, p);
   cudaError_t e = cudaGetLastError();
@@ -119,8 +119,8 @@ int launch_calib(const CUtensorMap& tq, const CUtensorMap& tk, const KernelParam
   return BSFA_OK;
 }
 
-// forward K1 (bsfa_fwd.cuh)
-template <int D, int GT>
+// forward K1 (bsfa_fwd3.cuh)
+template <int D, int GT, int BM>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
                cudaStream_t st) {
   using C = BSFA_FWD_CFG<D, GT>;
@@ -131,8 +131,8 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   const int smem = C::SMEM_BYTES;
 #define BSFA_GM(GM_, CA_)                                                                     \
   if (gm == GM_ && (p.causal != 0) == CA_) {                                                  \
-    kern = BSFA_FWD_KERNEL<D, GT, GM_, CA_>;                                                  \
-    rc = ensure_smem_attr<BSFA_FWD_KERNEL<D, GT, GM_, CA_>>(C::SMEM_BYTES);                   \
+    kern = BSFA_FWD_KERNEL<D, GT, GM_, CA_, BM>;                                              \
+    rc = ensure_smem_attr<BSFA_FWD_KERNEL<D, GT, GM_, CA_, BM>>(C::SMEM_BYTES);               \
   }
   BSFA_GM(0, true)
   BSFA_GM(0, false)
@@ -180,34 +180,45 @@ int launch_fwd7(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
 
 #endif
 
-int dispatch_fwd(int d, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+int dispatch_fwd(int d, int b_m, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                  const KernelParams& p, int grid, cudaStream_t st) {
-#define BSFA_FWD(D_, BN_) \
-  if (d == D_ && b_n == BN_) return launch_fwd<D_, 128 / BN_>(tq, tk, tv, p, grid, st);
-  BSFA_FWD(64, 64)
-  BSFA_FWD(128, 64)
-  BSFA_FWD(64, 128)
-  BSFA_FWD(128, 128)
+#define BSFA_FWD(D_, BM_, BN_) \
+  if (d == D_ && b_m == BM_ && b_n == BN_) return launch_fwd<D_, 128 / BN_, BM_>(tq, tk, tv, p, grid, st);
+  BSFA_FWD(64, 128, 64)
+  BSFA_FWD(128, 128, 64)
+  BSFA_FWD(64, 128, 128)
+  BSFA_FWD(128, 128, 128)
+  BSFA_FWD(64, 64, 64)
+  BSFA_FWD(128, 64, 64)
+  BSFA_FWD(64, 64, 128)
+  BSFA_FWD(128, 64, 128)
 #undef BSFA_FWD
-  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d b_n=%d", d, b_n);
+  return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d tiles %dx%d", d, b_m, b_n);
 }
 
-int dispatch_calib(int d, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const KernelParams& p, int grid,
-                   cudaStream_t st) {
-#define BSFA_CAL(D_, BN_) \
-  if (d == D_ && b_n == BN_) return launch_calib<D_, 128 / BN_>(tq, tk, p, grid, st);
-  BSFA_CAL(64, 64)
-  BSFA_CAL(128, 64)
-  BSFA_CAL(64, 128)
-  BSFA_CAL(128, 128)
+int dispatch_calib(int d, int b_m, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const KernelParams& p,
+                   int grid, cudaStream_t st) {
+#define BSFA_CAL(D_, BM_, BN_) \
+  if (d == D_ && b_m == BM_ && b_n == BN_) return launch_calib<D_, 128 / BN_, BM_>(tq, tk, p, grid, st);
+  BSFA_CAL(64, 128, 64)
+  BSFA_CAL(128, 128, 64)
+  BSFA_CAL(64, 128, 128)
+  BSFA_CAL(128, 128, 128)
+  BSFA_CAL(64, 64, 64)
+  BSFA_CAL(128, 64, 64)
+  BSFA_CAL(64, 64, 128)
+  BSFA_CAL(128, 64, 128)
 #undef BSFA_CAL
-  return fail(BSFA_ERR_INVALID, "no calibration kernel for head_dim=%d b_n=%d", d, b_n);
+  return fail(BSFA_ERR_INVALID, "no calibration kernel for head_dim=%d tiles %dx%d", d, b_m, b_n);
 }
 
+// b_m in {64, 128} x b_n in {64, 128}: the reference's 128x64 default and the
+// 64x64 / 64x128 / 128x128 tilings of its tests (tiling.py:26-32 admits any pair
+// where one size divides the other)
 int check_tiles(int b_m, int b_n) {
-  if (b_m != 128 || (b_n != 64 && b_n != 128))
-    return fail(BSFA_ERR_INVALID, "unsupported tiles %dx%d: the sm_100a kernel implements b_m=128, b_n in {64,128}",
-                b_m, b_n);
+  if ((b_m != 128 && b_m != 64) || (b_n != 64 && b_n != 128))
+    return fail(BSFA_ERR_INVALID,
+                "unsupported tiles %dx%d: the sm_100a kernel implements b_m in {64,128}, b_n in {64,128}", b_m, b_n);
   return BSFA_OK;
 }
 
@@ -331,7 +342,7 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
     return launch_fwd7<1>(tq, tk, tv, p, (int)(2 * grid), reinterpret_cast<cudaStream_t>(stream));
   }
 #endif
-  return dispatch_fwd(d, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch_fwd(d, a->b_m, a->b_n, tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
@@ -347,8 +358,12 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
     return fail(BSFA_ERR_INVALID, "calibration supports at most %d key blocks per row", CCfg<64, 2>::MAXA);
   if (a->num_levels < 1 || a->num_levels > 16) return fail(BSFA_ERR_INVALID, "1..16 k levels supported");
   if (a->layer < 0 || a->layer >= a->num_layers) return fail(BSFA_ERR_INVALID, "bad layer %d", a->layer);
-  if (a->seq_len / a->b_m > a->num_positions)
-    return fail(BSFA_ERR_INVALID, "sample has %d positions > accumulator %d", a->seq_len / a->b_m, a->num_positions);
+  const int valid = a->valid_len > 0 ? a->valid_len : a->seq_len;
+  if (valid > a->seq_len || valid % a->b_m || valid % a->b_n)
+    return fail(BSFA_ERR_INVALID, "valid_len %d must be <= seq_len %d and a multiple of b_m and b_n", valid,
+                a->seq_len);
+  if (valid / a->b_m > a->num_positions)
+    return fail(BSFA_ERR_INVALID, "sample has %d positions > accumulator %d", valid / a->b_m, a->num_positions);
   if (!a->q || !a->k || !a->finite_sum || !a->finite_cnt || !a->neg_cnt || !a->pos_cnt || !a->tie_counts)
     return fail(BSFA_ERR_INVALID, "null pointer");
 
@@ -366,7 +381,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   p.heads_kv = a->heads_kv;
   p.group = a->heads_q / a->heads_kv;
   p.seq_len = n;
-  p.valid_len = n;
+  p.valid_len = valid;  // the sample's reference grid; rows past it are kernel padding
   p.num_q_tiles = n / 128;
   p.num_steps = n / 128;
   p.gate_cols = n / a->b_n;
@@ -393,7 +408,7 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   const int nq = 2;
   const int grid = p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2) : (a->heads_q / nq) * p.num_q_tiles;
   (void)nq;
-  return dispatch_calib(d, a->b_n, tq, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
+  return dispatch_calib(d, a->b_m, a->b_n, tq, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

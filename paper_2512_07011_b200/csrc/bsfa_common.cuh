@@ -102,4 +102,45 @@ __device__ __forceinline__ int step_static_bits(int gate_mode, int window, int j
   return -1;  // ThresholdGate / RunningMaxGate: voted
 }
 
+// b_m = 64 (a 128-row query tile holds query blocks 2t and 2t+1): the gate
+// tiles x of step j for 64-row query block `blk` (tiling.py:50-65, engine.py:
+// 152-174): `reach` = causally reachable, `front` = frontier (always kept,
+// causal mask on its elements), `smask` = decided without a vote, `sval` =
+// their keep bits.  Gate columns / blocks past the reference's padded grid
+// (kernel padding to 128 rows) are computed like any other and only left out
+// of the counters and the cropped trace.
+struct StepBits64 {
+  uint32_t reach, front, smask, sval;
+};
+template <int GT>
+__device__ __forceinline__ StepBits64 step_bits64(int gate_mode, int window, bool causal, int j, int blk) {
+  constexpr int BN = 128 / GT;
+  const int f_lo = (blk * 64) / BN, f_hi = (blk * 64 + 64 + BN - 1) / BN;
+  StepBits64 r{0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int x = 0; x < GT; ++x) {
+    const int g = j * GT + x;
+    const uint32_t bit = 1u << x;
+    if (causal && g >= f_hi) {  // unreachable: statically not kept
+      r.smask |= bit;
+      continue;
+    }
+    r.reach |= bit;
+    if (g >= f_lo && g < f_hi) {
+      r.front |= bit;
+      r.smask |= bit;
+      r.sval |= bit;
+    } else if (gate_mode == kGateDense) {
+      r.smask |= bit;
+      r.sval |= bit;
+    } else if (gate_mode == kGateFrontier) {
+      r.smask |= bit;
+    } else if (gate_mode == kGateWindow) {  // gates.py:96-98 with b_m = 64
+      r.smask |= bit;
+      if ((g + 1) * BN > blk * 64 - window && g * BN < (blk + 1) * 64) r.sval |= bit;
+    }  // ThresholdGate / RunningMaxGate: voted
+  }
+  return r;
+}
+
 }  // namespace bsfa

@@ -128,7 +128,14 @@ struct FCfg3 {
 // FrontierOnlyGate, SlidingWindowGate: no vote), 2 RunningMaxGate (voted).  GM and
 // CAUSAL are template parameters so the per-step softmax code carries no
 // runtime gate/causality branches (smaller loop body, fewer taken branches).
-template <int D, int GT, int GM, bool CAUSAL>
+// BM: the reference's query block b_m.  128: a query tile is one block.  64: a
+// 128-row tile holds blocks 2t (rows 0-63, warps 0-1 of the tile) and 2t+1
+// (rows 64-127, warps 2-3); each block has its own threshold, frontier and
+// gate decisions (one vote word per warp, combined per block), a 64-key unit
+// is fetched and multiplied when either block of either tile keeps it, and a
+// block that skipped a unit the other block kept writes zeros into its P rows
+// (its O, max and row sum are untouched).
+template <int D, int GT, int GM, bool CAUSAL, int BM = 128>
 __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     bsfa_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
@@ -202,9 +209,23 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
   const int nsteps = ns_a[0];  // tile 0 is never the shorter one
   const int gate_mode = p.gate_mode;
   const int window = p.gate_window;
+  static_assert(BM == 128 || BM == 64, "b_m in {64, 128}");
+  // b_m = 64: the reference grid is padded to lcm(64, b_n) <= 128, the kernel's
+  // to 128; gate columns / query blocks past the reference grid are not counted
+  constexpr int LCM = BM == 64 ? (GT == 1 ? 128 : 64) : 128;
+  const int n_ref = (p.valid_len + LCM - 1) / LCM * LCM;
+  const int kv_valid = n_ref / (128 / GT);
+  const int q_valid = n_ref / BM;
+  // b_m = 64: statics of both blocks of tile s at step j; the union of the two
+  // blocks' keeps from the tile's four vote words
+  auto bits64 = [&](int j, int qi, int hf) { return step_bits64<GT>(gate_mode, window, CAUSAL, j, 2 * qi + hf); };
+  auto voted64 = [&](const StepBits64& a) { return a.reach & ~a.smask; };
+  auto union64 = [&](const StepBits64& a0, const StepBits64& a1, const uint4 w) {
+    return (a0.sval | (voted64(a0) & (w.x | w.y))) | (a1.sval | (voted64(a1) & (w.z | w.w)));
+  };
   // statically known decision bits of step j for query block qi (-1: voted)
   // the V producer reads ThresholdGate decisions straight from the vote words
-  constexpr bool VP = GM == 0 && GT == 2 && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
+  constexpr bool VP = GM == 0 && (GT == 2 || BM == 64) && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
   constexpr bool SNB = !BSFA_FWD3_SPLIT && (BSFA_SFREE_NB == 1 || (BSFA_SFREE_NB == 2 && GM == 1));
   auto sbits = [&](int j, int qi) -> int {
     if constexpr (GM == 1) return step_static_bits<GT>(gate_mode, window, j, qi);
@@ -293,9 +314,28 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           if (j >= ns_a[s]) continue;
-          const int sbs = sbits(j, qi_a[s]);
+          const int sbs = BM == 64 ? 0 : sbits(j, qi_a[s]);
           uint32_t w;
-          if (sbs >= 0) {
+          if constexpr (BM == 64) {
+            const int qs = s ? qi_a[1] : qi_a[0];
+            const StepBits64 a0 = bits64(j, qs, 0), a1 = bits64(j, qs, 1);
+            if (GM == 1 || !(voted64(a0) | voted64(a1))) {
+              w = a0.sval | a1.sval;
+            } else if constexpr (VP) {
+              named_bar_sync(1 + s, 160);
+              w = union64(a0, a1, lds_u128(vote_sm + (s * 2 + int(dn_a[s] & 1u)) * 16));
+              ++dn_a[s];  // (vote rounds of tile s)
+            } else {
+              const uint32_t slot_addr = dec_sm + (s * DQ + int(dn_a[s] % DQ)) * 4;
+              const uint32_t tag = dn_a[s] + 1;
+              uint32_t word = ld_volatile_u32(slot_addr);
+              while ((word >> 4) != tag) word = ld_volatile_u32(slot_addr);
+              w = word & 0xFu;
+              ++dn_a[s];
+              __syncwarp();
+              if (lane == 0) st_volatile_u32(dec_cons + 4 * s, dn_a[s]);
+            }
+          } else if (sbs >= 0) {
             w = uint32_t(sbs);
           } else if constexpr (VP) {
             named_bar_sync(1 + s, 160);  // the tile's vote (128 softmax threads + this warp)
@@ -406,11 +446,25 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       // PV_s(j), part 1 (after p_full): the tile's decision -> 64-key halves kept
       // and their V unit numbers (units numbered in the producer's fetch order)
       auto pv_decide = [&](int s, int j) -> uint32_t {
-        const int sb = sbits(j, s ? qi_a[1] : qi_a[0]);  // (selects: s may be a runtime value)
+        const int sb = BM == 64 ? 0 : sbits(j, s ? qi_a[1] : qi_a[0]);  // (selects: s may be a runtime value)
         tc_fence_after();
         if (lane == 0) trace(6, s, j);
         uint32_t bits;
-        if (sb >= 0) {
+        if constexpr (BM == 64) {
+          const int qs = s ? qi_a[1] : qi_a[0];
+          const StepBits64 a0 = bits64(j, qs, 0), a1 = bits64(j, qs, 1);
+          if (GM == 1 || !(voted64(a0) | voted64(a1))) {
+            bits = a0.sval | a1.sval;
+          } else if constexpr (VP) {
+            const unsigned n = s ? dn_m[1] : dn_m[0];
+            bits = union64(a0, a1, lds_u128(vote_sm + (s * 2 + int(n & 1u)) * 16));
+            if (s) ++dn_m[1]; else ++dn_m[0];
+          } else {
+            const unsigned n = s ? dn_m[1] : dn_m[0];
+            bits = ld_volatile_u32(dec_sm + (s * DQ + int(n % DQ)) * 4) & 0xFu;
+            if (s) ++dn_m[1]; else ++dn_m[0];
+          }
+        } else if (sb >= 0) {
           bits = uint32_t(sb);
         } else if constexpr (VP) {
           // the vote words of step j: rewritten only at step j + 2, whose vote
@@ -478,7 +532,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         if (pv_role && j < ns_a[1]) issue_pv(1, j);
         if (pv_role) end_pv_step();
       }
-      if (pv_role && lane == 0 && p.counters) {
+      if (BM == 128 && pv_role && lane == 0 && p.counters) {  // (b_m = 64: counted per block by the softmax)
         atomicAdd(&p.counters[0], (unsigned long long)(ns_a[0] + ns_a[1]) * GT);
         atomicAdd(&p.counters[1], kept_m);
       }
@@ -514,11 +568,16 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     const float rescale_raw = p.rescale_raw;
     const int valid_len = p.valid_len;
 
+    // b_m = 64: this thread's query block (rows 0-63 / 64-127 of the tile)
+    const int hf = BM == 64 ? (r >> 6) : 0;
+    const int blk = BM == 64 ? 2 * qi_s + hf : qi_s;
     float T = 0.f;
     if constexpr (GM == 0) {
-      const int pos = qi_s < p.thr_positions - 1 ? qi_s : p.thr_positions - 1;
+      const int pos = blk < p.thr_positions - 1 ? blk : p.thr_positions - 1;
       T = p.thr[(long long)hq * p.thr_positions + pos];  // thresholds.py:87
     }
+    unsigned nb = 0;                          // b_m = 64: vote rounds of this tile
+    unsigned long long reach_cnt = 0, kept_cnt = 0;  // b_m = 64: this block's counters
     const float lam = p.gate_lambda;
     float m_true = -INFINITY;  // exact running row max (RunningMaxGate), raw units
     float m_ref = -INFINITY;   // raw reference max of this row over its kept tiles
@@ -533,7 +592,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
     };
     unsigned dn = 0;
-    int8_t* drow = p.decisions ? p.decisions + (((long long)b * p.heads_q + hq) * p.num_q_tiles + qi_s) * p.gate_cols
+    int8_t* drow = p.decisions ? p.decisions + (((long long)b * p.heads_q + hq) * (p.num_q_tiles * (128 / BM)) + blk) *
+                                                   p.gate_cols
                                : nullptr;
 
     for (int j = 0; j < nst; ++j) {
@@ -604,68 +664,143 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
 
       // ---- gate decision, OR over the tile's 128 rows in the barrier hardware
-      uint32_t bits;
-      if (GM == 1 || sb >= 0) {
-        bits = uint32_t(sb);
-      } else if constexpr (GM == 0) {
-        // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
-        if constexpr (GT == 2 && BSFA_VOTE1) {
-          // both gate tiles in ONE barrier: OR within the warp (REDUX), one word
-          // per warp in shared memory (parity double-buffered: a warp reaches
-          // step j+2's store only after every warp passed step j+1's barrier,
-          // i.e. read step j's words), bar.sync, OR of the four words
-          const uint32_t v = (mx[0] * scale > T ? 1u : 0u) | (mx[1] * scale > T ? 2u : 0u);
-          const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
-          const uint32_t slot = vote_sm + (s * 2 + (j & 1)) * 16;
-          if (lane == 0) sts_u32(slot + wq * 4, wv);
-          named_bar_sync(1 + s, VP ? 160 : 128);
-          const uint4 all = lds_u128(slot);
-          bits = all.x | all.y | all.z | all.w;
-        } else {
-          bits = 0;
-#pragma unroll
-          for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
-        }
-      } else {
-        // RunningMaxGate (gates.py:101-118): gate tiles in key order, each judged
-        // against the running max before it is merged
-        bits = 0;
-        float mrun = m_true;
-#pragma unroll
-        for (int x = 0; x < GT; ++x) {
-          const uint32_t k = named_bar_red_or(1 + s, 128, (mx[x] - mrun) * scale >= lam ? 1u : 0u);
-          bits |= k << x;
-          if (k) mrun = fmaxf(mrun, mx[x]);
-        }
-      }
-      if constexpr (GM == 2) {
-#pragma unroll
-        for (int x = 0; x < GT; ++x)
-          if ((bits >> x) & 1u) m_true = fmaxf(m_true, mx[x]);
-      }
-      if (BSFA_TRACE && r == 0) {
-        asm volatile("" ::"r"(bits));
-        trace(9, s, j);
-      }
-      // bookkeeping spread over the tile's warps (every thread holds `bits`), so
-      // no single warp lags into the next vote
-      if (GM != 1 && !VP && r == 64 && sb < 0) {
-        // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
-        // few steps at most -- it gates the PVs -- so this never spins in practice)
-        if (dn >= DQ)
-          while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
+      uint32_t bits;   // this thread's query block's keeps (gate tiles of the step)
+      uint32_t ubits;  // keeps of either block of the tile (b_m = 64; = bits otherwise)
+      if constexpr (BM == 128) {
+        if (GM == 1 || sb >= 0) {
+          bits = uint32_t(sb);
+        } else if constexpr (GM == 0) {
+          // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
+          if constexpr (GT == 2 && BSFA_VOTE1) {
+            // both gate tiles in ONE barrier: OR within the warp (REDUX), one word
+            // per warp in shared memory (parity double-buffered: a warp reaches
+            // step j+2's store only after every warp passed step j+1's barrier,
+            // i.e. read step j's words), bar.sync, OR of the four words
+            const uint32_t v = (mx[0] * scale > T ? 1u : 0u) | (mx[1] * scale > T ? 2u : 0u);
+            const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
+            const uint32_t slot = vote_sm + (s * 2 + (j & 1)) * 16;
+            if (lane == 0) sts_u32(slot + wq * 4, wv);
+            named_bar_sync(1 + s, VP ? 160 : 128);
+            const uint4 all = lds_u128(slot);
+            bits = all.x | all.y | all.z | all.w;
+          } else {
+            bits = 0;
+  #pragma unroll
+            for (int x = 0; x < GT; ++x) bits |= named_bar_red_or(1 + s, 128, mx[x] * scale > T ? 1u : 0u) << x;
           }
-        st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
-      }
-      if (drow && r == 0) {
+        } else {
+          // RunningMaxGate (gates.py:101-118): gate tiles in key order, each judged
+          // against the running max before it is merged
+          bits = 0;
+          float mrun = m_true;
+  #pragma unroll
+          for (int x = 0; x < GT; ++x) {
+            const uint32_t k = named_bar_red_or(1 + s, 128, (mx[x] - mrun) * scale >= lam ? 1u : 0u);
+            bits |= k << x;
+            if (k) mrun = fmaxf(mrun, mx[x]);
+          }
+        }
+        if constexpr (GM == 2) {
+  #pragma unroll
+          for (int x = 0; x < GT; ++x)
+            if ((bits >> x) & 1u) m_true = fmaxf(m_true, mx[x]);
+        }
+        if (BSFA_TRACE && r == 0) {
+          asm volatile("" ::"r"(bits));
+          trace(9, s, j);
+        }
+        // bookkeeping spread over the tile's warps (every thread holds `bits`), so
+        // no single warp lags into the next vote
+        if (GM != 1 && !VP && r == 64 && sb < 0) {
+          // ring slot reuse: the producer consumed decision dn - DQ (it lags by a
+          // few steps at most -- it gates the PVs -- so this never spins in practice)
+          if (dn >= DQ)
+            while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
+            }
+          st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | bits);
+        }
+        if (drow && r == 0) {
+  #pragma unroll
+          for (int x = 0; x < GT; ++x)
+            drow[j * GT + x] = j == qi_s ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+        }
+        if (GM != 1 && sb < 0) ++dn;
+        ubits = bits;
+      } else {
+        // b_m = 64: statics per block; one vote round per gate class decision,
+        // a word per warp (warps 0-1: block 2t, warps 2-3: block 2t+1)
+        const StepBits64 a0 = bits64(j, qi_s, 0), a1 = bits64(j, qi_s, 1);
+        const StepBits64 am = hf ? a1 : a0;
+        const uint32_t v0 = voted64(a0), v1 = voted64(a1), vm = voted64(am);
+        uint32_t b0 = a0.sval, b1 = a1.sval;
+        const bool voted_step = GM != 1 && (v0 | v1) != 0;
+        if constexpr (GM == 0) {
+          if (voted_step) {
+            uint32_t v = 0;
 #pragma unroll
-        for (int x = 0; x < GT; ++x)
-          drow[j * GT + x] = j == qi_s ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+            for (int x = 0; x < GT; ++x)
+              if (((vm >> x) & 1u) && mx[x] * scale > T) v |= 1u << x;  // gates.py:77-78
+            const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
+            const uint32_t slot = vote_sm + (s * 2 + int(nb & 1u)) * 16;
+            if (lane == 0) sts_u32(slot + wq * 4, wv);
+            named_bar_sync(1 + s, VP ? 160 : 128);
+            const uint4 all = lds_u128(slot);
+            ++nb;
+            b0 |= v0 & (all.x | all.y);
+            b1 |= v1 & (all.z | all.w);
+          }
+        } else if constexpr (GM == 2) {
+          // RunningMaxGate (gates.py:101-118): gate tiles in key order, each
+          // judged against this row's running max before it is merged
+          float mrun = m_true;
+#pragma unroll
+          for (int x = 0; x < GT; ++x) {
+            if (((v0 | v1) >> x) & 1u) {
+              const uint32_t pv = (((vm >> x) & 1u) && (mx[x] - mrun) * scale >= lam) ? (1u << x) : 0u;
+              const uint32_t wv = __reduce_or_sync(0xffffffffu, pv);
+              const uint32_t slot = vote_sm + (s * 2 + int(nb & 1u)) * 16;
+              if (lane == 0) sts_u32(slot + wq * 4, wv);
+              named_bar_sync(1 + s, 128);
+              const uint4 all = lds_u128(slot);
+              ++nb;
+              b0 |= v0 & (all.x | all.y) & (1u << x);
+              b1 |= v1 & (all.z | all.w) & (1u << x);
+            }
+            if ((((hf ? b1 : b0)) >> x) & 1u) mrun = fmaxf(mrun, mx[x]);
+          }
+        }
+        bits = hf ? b1 : b0;
+        ubits = b0 | b1;
+        if constexpr (GM == 2) {
+#pragma unroll
+          for (int x = 0; x < GT; ++x)
+            if ((bits >> x) & 1u) m_true = fmaxf(m_true, mx[x]);
+        }
+        if (GM != 1 && !VP && r == 64 && voted_step) {  // the union for the V producer and the MMA warp
+          if (dn >= DQ)
+            while (ld_volatile_u32(dec_cons + 4 * s) < dn - DQ + 1) {
+            }
+          st_volatile_u32(dec_sm + (s * DQ + int(dn % DQ)) * 4, ((dn + 1) << 4) | ubits);
+        }
+        if (voted_step) ++dn;
+        if ((r & 63) == 0) {  // one thread per query block: trace row and counters
+          if (drow) {
+#pragma unroll
+            for (int x = 0; x < GT; ++x)
+              if ((am.reach >> x) & 1u)
+                drow[j * GT + x] = ((am.front >> x) & 1u) ? int8_t(2) : (((bits >> x) & 1u) ? int8_t(3) : int8_t(1));
+          }
+          if (blk < q_valid) {  // the reference grid only
+            const int cols = kv_valid - j * GT;
+            const uint32_t cm = cols >= GT ? (1u << GT) - 1 : (cols > 0 ? (1u << cols) - 1 : 0u);
+            reach_cnt += __popc(am.reach & cm);
+            kept_cnt += __popc(bits & am.reach & cm);
+          }
+        }
       }
-      if (GM != 1 && sb < 0) ++dn;
       if (r == 0) trace(2, s, j);
       const uint32_t p_bar = p_full + 16 * s + 8 * (j & 1);
-      if (bits == 0) {
+      if (ubits == 0) {
         __syncwarp();
         if (lane == 0) mbar_arrive(p_bar);
         if (r == 0) {
@@ -674,7 +809,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         }
         continue;
       }
-      const uint32_t hb = GT == 2 ? bits : 3u;
+      const uint32_t hb = GT == 2 ? bits : (bits ? 3u : 0u);  // 64-key units this row keeps
+      const uint32_t hbu = GT == 2 ? ubits : 3u;               // units the tile's PVs read (b_m = 64: either block)
 
       float m_step = -INFINITY;
 #pragma unroll
@@ -746,6 +882,13 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
           }
           pv_wait();  // the last PVs have read P_s
           tmem_st32(p_row + hh * 32, pk);
+        } else if (BM == 64 && ((hbu >> hh) & 1u)) {
+          // the other block of the tile kept this unit: zero rows for this block
+          uint32_t z[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) z[c] = 0u;
+          pv_wait();
+          tmem_st32(p_row + hh * 32, z);
         }
         if (hh == 0 && r == 0) trace(3, s, j);
       }
@@ -759,7 +902,7 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       }
       const uint64_t acc = fadd2(acc0, acc1);
       l_sum = l_sum * alpha + (f2_lo(acc) + f2_hi(acc));
-      o_valid = true;
+      if (BM == 128 || bits) o_valid = true;
       if (r == 0) trace(4, s, j);
     }
 
@@ -789,6 +932,10 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
     p.lse[((long long)b * p.heads_q + hq) * p.seq_len + row] = m_ref * scale + logf(l_sum);
     if (r == 0) trace(12, 1, s);  // (debug builds) tile s's epilogue stores issued
     if (bad && p.status) atomicOr(p.status, 1);
+    if (BM == 64 && (r & 63) == 0 && p.counters && (reach_cnt | kept_cnt)) {
+      atomicAdd(&p.counters[0], reach_cnt);
+      atomicAdd(&p.counters[1], kept_cnt);
+    }
     tc_fence_before();
     named_bar_arrive(15, C::NUM_THREADS);
     return;

@@ -342,7 +342,7 @@ def test_unsupported_gate_and_tiles_refused(bsfa):
     with pytest.raises(bsfa.ConfigurationError):
         bsfa.flash_forward(inp, bsfa.TileConfig(128, 64), Sliding())
     with pytest.raises(bsfa.ConfigurationError):
-        bsfa.flash_forward(inp, bsfa.TileConfig(64, 64), bsfa.dense_gate())
+        bsfa.flash_forward(inp, bsfa.TileConfig(64, 32), bsfa.dense_gate())
 
 
 # ------------------------------------------------------------------ paper baseline gates

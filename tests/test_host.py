@@ -52,7 +52,7 @@ def test_struct_layout_matches_header():
 def test_invalid_arguments_are_rejected_without_touching_the_gpu():
     lib = _lib.load_library()
     a = _lib.FwdArgs()
-    a.b_m, a.b_n, a.head_dim = 64, 64, 64
+    a.b_m, a.b_n, a.head_dim = 64, 32, 64
     assert lib.bsfa_fwd(ctypes.byref(a), None) == _lib.BSFA_ERR_INVALID
     assert b"unsupported tiles" in lib.bsfa_last_error()
     a.b_m, a.b_n, a.head_dim = 128, 64, 96
@@ -85,7 +85,9 @@ def test_tiling_matches_reference_kats():
         with pytest.raises(ConfigurationError):
             bsfa.TileConfig(*bad)
     assert bsfa.kernel_supports(t) and bsfa.kernel_supports(bsfa.TileConfig(128, 128))
-    assert not bsfa.kernel_supports(bsfa.TileConfig(64, 64))
+    assert bsfa.kernel_supports(bsfa.TileConfig(64, 64)) and bsfa.kernel_supports(bsfa.TileConfig(64, 128))
+    assert not bsfa.kernel_supports(bsfa.TileConfig(64, 32)) and not bsfa.kernel_supports(bsfa.TileConfig(256, 128))
+    assert bsfa.kernel_len(192, bsfa.TileConfig(64, 64)) == 256 and bsfa.kernel_len(200, bsfa.TileConfig(64, 128)) == 256
 
 
 # ------------------------------------------------------------------ thresholds
