@@ -79,6 +79,13 @@
 #ifndef BSFA_SFREE_NB
 #define BSFA_SFREE_NB 2
 #endif
+#ifndef BSFA_MAXTREE
+#define BSFA_MAXTREE 0
+#endif
+// the score row as one 32x32b.x128 tcgen05.ld (1) or four x32 loads (0)
+#ifndef BSFA_LD128
+#define BSFA_LD128 0
+#endif
 
 namespace bsfa {
 
@@ -605,8 +612,12 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
       if (r == 0) trace(0, s, j);
       tc_fence_after();
       uint32_t sv[128];
+      if (BSFA_LD128) {
+        tmem_ld128(s_row, sv);
+      } else {
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
+        for (int c = 0; c < 128; c += 32) tmem_ld32(s_row + c, &sv[c]);
+      }
       tmem_wait_ld();
       tc_fence_before();
       if (SNB) {
@@ -630,11 +641,26 @@ __global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
         for (int c = 0; c < 128; ++c)
           if (j * 128 + c >= valid_len) sv[c] = __float_as_uint(-INFINITY);
       }
-      // row max per 64-key half (three-input FMNMX, four chains each)
+      // row max per 64-key half (three-input FMNMX, four chains each; BSFA_MAXTREE:
+      // a balanced ternary tree, 4 levels deep instead of 16)
       float mh[2];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const uint32_t* x = sv + hh * 64;
+        if (BSFA_MAXTREE) {
+          float l1[22];
+#pragma unroll
+          for (int t = 0; t < 21; ++t)
+            l1[t] = fmax3(__uint_as_float(x[3 * t]), __uint_as_float(x[3 * t + 1]), __uint_as_float(x[3 * t + 2]));
+          l1[21] = __uint_as_float(x[63]);
+          float l2[8];
+#pragma unroll
+          for (int t = 0; t < 7; ++t) l2[t] = fmax3(l1[3 * t], l1[3 * t + 1], l1[3 * t + 2]);
+          l2[7] = l1[21];
+          const float l3a = fmax3(l2[0], l2[1], l2[2]), l3b = fmax3(l2[3], l2[4], l2[5]);
+          mh[hh] = fmaxf(fmax3(l3a, l3b, l2[6]), l2[7]);
+          continue;
+        }
         float a0 = fmax3(__uint_as_float(x[0]), __uint_as_float(x[1]), __uint_as_float(x[2]));
         float a1 = fmax3(__uint_as_float(x[3]), __uint_as_float(x[4]), __uint_as_float(x[5]));
         float a2 = fmax3(__uint_as_float(x[6]), __uint_as_float(x[7]), __uint_as_float(x[8]));
