@@ -204,6 +204,12 @@ class Calibrator:
         a.finite_sum, a.finite_cnt = self.sum.data_ptr(), self.fin.data_ptr()
         a.neg_cnt, a.pos_cnt = self.neg.data_ptr(), self.pos.data_ptr()
         a.tie_counts = self.ties.data_ptr()
+        if block_maxima is not None:
+            want = (qd.shape[0], n_kern // self.tiles.b_m, n_kern // self.tiles.b_n)
+            if (tuple(block_maxima.shape) != want or block_maxima.dtype != torch.float32
+                    or block_maxima.device != qd.device or not block_maxima.is_contiguous()):
+                raise InvalidInputError(f"block_maxima must be contiguous fp32 {want} on {qd.device}, got "
+                                        f"{block_maxima.dtype} {tuple(block_maxima.shape)} on {block_maxima.device}")
         a.block_maxima = block_maxima.data_ptr() if block_maxima is not None else None
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device).cuda_stream
