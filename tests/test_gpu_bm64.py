@@ -222,3 +222,22 @@ def test_bm64_topk_round_trip(bsfa):
                 a = orc.off_frontier(i, 64, 64)
                 kept = int((dec[h, i, :a] == orc.KEPT).sum())
                 assert kept == min(kk, a), (kk, h, i, kept)
+
+
+def test_block_maxima_buffer_validated(bsfa):
+    """A caller's block_maxima buffer must match the kernel grid (kernel_len rows) before the launch."""
+    rng = np.random.default_rng(3)
+    n, d = 448, 64
+    q = _inputs(rng, n, d, (2,))
+    k = _inputs(rng, n, d, (1,))
+    tiles = bsfa.TileConfig(64, 64)
+    cal = bsfa.Calibrator([1], tiles, 1, 2, n, d, device="cuda")
+    nk = bsfa.kernel_len(n, tiles)
+    with pytest.raises(bsfa.InvalidInputError):
+        cal.add_layer(0, 0, q, k, block_maxima=torch.zeros((2, n // 64, n // 64), device="cuda"))
+    ok = torch.full((2, nk // 64, nk // 64), float("nan"), device="cuda")
+    cal.add_layer(0, 0, q, k, block_maxima=ok)
+    ref = orc.block_maxima(q[1], k[0], 64, 64)
+    got = ok[1].cpu().numpy()
+    for p, vals in enumerate(ref):
+        np.testing.assert_allclose(np.sort(got[p, :len(vals)])[::-1], vals, atol=1e-4)
