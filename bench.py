@@ -19,7 +19,10 @@ Reported (one JSON line on rank 0):
               buffers, H2D of Q/K/V and D2H of O inside the timed region
   roofline    tensor-core bound; achieved = F_exec per launch / mean launch
               time vs the measured bf16 peak (MEASURED_PEAKS.json)
-  cpu_baseline  the oracle port of the reference engine on one host core
+  cpu_baseline  one full head of the workload through the unmodified reference
+              package (baseline/_ref) on one host core -- kind "reference";
+              the oracle port on sampled query blocks when the package is
+              absent or the sequence is longer than 32K -- kind "port"
   dense_*     the same kernel with the DenseGate (T = -inf), for speedup
   interleaved BSFA and dense timed ABAB after the timed region (steady state)
 Multi-GPU (torchrun, BASELINE configs[3]): 128K, kv-head groups sharded over
