@@ -241,3 +241,37 @@ def test_block_maxima_buffer_validated(bsfa):
     got = ok[1].cpu().numpy()
     for p, vals in enumerate(ref):
         np.testing.assert_allclose(np.sort(got[p, :len(vals)])[::-1], vals, atol=1e-4)
+
+
+def test_bm64_torch_ops(bsfa):
+    """torch.ops.bsfa.fwd / blockmax / calib_select at 64x64 on an odd block count: the op equals
+    attention() bit for bit, the block maxima equal the oracle's, the selected cutoffs its calibrate()."""
+    rng = np.random.default_rng(9)
+    n, d = 704, 128
+    q = _inputs(rng, n, d, (1, 2))
+    k = _inputs(rng, n, d, (1, 1))
+    v = _inputs(rng, n, d, (1, 1))
+    dev = lambda x: torch.from_numpy(x).cuda().to(torch.bfloat16)  # noqa: E731
+    tiles = bsfa.TileConfig(64, 64)
+    thr = np.stack([_median_thresholds(q[0, h], k[0, 0], 64, 64, rng, n) for h in range(2)])
+    t = bsfa.ThresholdTensor(values=thr[None, None], k_levels=(2,), n_max=n, b_m=64, b_n=64)
+    ref = bsfa.attention(dev(q), dev(k), dev(v), tiles=tiles, thresholds=t, k_level=2, return_trace=True)
+    o, lse, cnt, dec = torch.ops.bsfa.fwd(dev(q), dev(k), dev(v), torch.from_numpy(thr).cuda(), True, 64, 64,
+                                          bsfa.reference_scale(d), True)
+    assert torch.equal(o, ref.o) and torch.equal(lse, ref.lse) and torch.equal(dec, ref.decisions)
+    assert torch.equal(cnt[:2], ref.counters[:2])
+    bm = torch.ops.bsfa.blockmax(dev(q), dev(np.repeat(k, 2, axis=1)), 64, 64)
+    assert tuple(bm.shape) == (1, 2, n // 64, n // 64)
+    for h in range(2):
+        prof = orc.block_maxima(q[0, h], k[0, 0], 64, 64)
+        got = bm[0, h].cpu().numpy()
+        for p, vals in enumerate(prof):
+            np.testing.assert_allclose(np.sort(got[p, :len(vals)])[::-1], vals, atol=1e-4)
+    levels = [1, 3]
+    sel, _ = torch.ops.bsfa.calib_select(bm, levels, 64, 64)
+    ref_vals, _, _ = orc.calibrate([(0, q, k)], levels, 64, 64)
+    got = sel.cpu().numpy()[:, 0]  # [levels, heads, positions]
+    want = ref_vals[:, 0]
+    fin = np.isfinite(want)
+    np.testing.assert_array_equal(np.isfinite(got), fin)
+    assert np.abs(got[fin] - want[fin]).max() <= 1e-4

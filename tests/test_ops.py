@@ -19,3 +19,13 @@ def test_ops_registered_with_fake_shapes():
         assert bm.shape == (2, 4, 8, 16) and bm.dtype == torch.float32
         t, ties = torch.ops.bsfa.calib_select(bm, [0, 3, 7], 128, 64)
         assert t.shape == (3, 2, 4, 8) and ties.shape == (3,)
+
+
+def test_ops_fake_shapes_bm64():
+    """b_m = 64: the reference grid of n = 1000 is 1024 rows (lcm 64 / 128), 16 query blocks."""
+    with FakeTensorMode():
+        q = torch.empty(1, 2, 1000, 128, dtype=torch.bfloat16, device="cuda")
+        thr = torch.empty(2, 16, device="cuda")
+        _, _, _, dec = torch.ops.bsfa.fwd(q, q, q, thr, True, 64, 64, 0.088, True)
+        assert dec.shape == (1, 2, 16, 16)
+        assert torch.ops.bsfa.blockmax(q, q, 64, 128).shape == (1, 2, 16, 8)
