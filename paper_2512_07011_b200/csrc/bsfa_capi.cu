@@ -123,16 +123,18 @@ int launch_calib(const CUtensorMap& tq, const CUtensorMap& tk, const KernelParam
 template <int D, int GT, int BM>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
                cudaStream_t st) {
-  using C = BSFA_FWD_CFG<D, GT>;
-  // gate class and causality are template parameters of the forward kernel
+  // gate class and causality are template parameters of the forward kernel;
+  // the shared-memory rings (hence the size) depend on the gate class
   const int gm = p.gate_mode == BSFA_GATE_THRESHOLD ? 0 : (p.gate_mode == BSFA_GATE_RUNMAX ? 2 : 1);
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) = nullptr;
   int rc = BSFA_OK;
-  const int smem = C::SMEM_BYTES;
+  int smem = 0;
+  constexpr int threads = BSFA_FWD_CFG<D, GT>::NUM_THREADS;
 #define BSFA_GM(GM_, CA_)                                                                     \
   if (gm == GM_ && (p.causal != 0) == CA_) {                                                  \
     kern = BSFA_FWD_KERNEL<D, GT, GM_, CA_, BM>;                                              \
-    rc = ensure_smem_attr<BSFA_FWD_KERNEL<D, GT, GM_, CA_, BM>>(C::SMEM_BYTES);               \
+    smem = BSFA_FWD_CFG<D, GT, GM_>::SMEM_BYTES;                                              \
+    rc = ensure_smem_attr<BSFA_FWD_KERNEL<D, GT, GM_, CA_, BM>>(smem);                        \
   }
   BSFA_GM(0, true)
   BSFA_GM(0, false)
@@ -143,7 +145,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
 #undef BSFA_GM
   if (rc) return rc;
   if (grid == 0) return BSFA_OK;
-  kern<<<grid, C::NUM_THREADS, smem, st>>>(tq, tk, tv, p);
+  kern<<<grid, threads, smem, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bsfa forward launch");
   return BSFA_OK;

@@ -89,7 +89,12 @@
 
 namespace bsfa {
 
-template <int D, int GT>
+// Ring depths per gate class (measured, profiles/r02_s3_ab_rings.jsonl): the
+// voted kernels (GM 0 / 2) fetch V only after a vote, so a deeper K ring (6
+// chunks = 3 steps) beats a deeper V ring (BSFA 1.1 % faster at 32K, 0.5 % at
+// 128K); the statically gated ones (dense, frontier, window) prefetch V and
+// keep the 6-unit V ring (dense 1.1-1.4 % faster with it).
+template <int D, int GT, int GM = 1>
 struct FCfg3 {
   static constexpr int BN = 128 / GT;           // gate tile width (reference b_n)
   static constexpr int NCH = D / 64;            // 64-column swizzle atoms along head_dim
@@ -98,8 +103,8 @@ struct FCfg3 {
   static constexpr int K_CHUNK = 128 * 128;     // 128 keys x 64 columns, bf16
   static constexpr int V_UNIT = 64 * D * 2;     // 64 keys of V
   static constexpr int V_ATOM = 64 * 128;       // 64 keys x 64 columns
-  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : 4;
-  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 128 ? 6 : 8);
+  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : (GM == 1 ? 4 : 6);
+  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 128 ? (GM == 1 ? 6 : 4) : 8);
   static constexpr int DQ = 8;                  // decision ring depth (V producer)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
@@ -143,10 +148,10 @@ struct FCfg3 {
 // block that skipped a unit the other block kept writes zeros into its P rows
 // (its O, max and row sum are untouched).
 template <int D, int GT, int GM, bool CAUSAL, int BM = 128>
-__global__ void __launch_bounds__(FCfg3<D, GT>::NUM_THREADS, 1)
+__global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
     bsfa_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
-  using C = FCfg3<D, GT>;
+  using C = FCfg3<D, GT, GM>;
   constexpr int KC = C::KC, VS = C::VS, DQ = C::DQ, NCH = C::NCH;
 
   extern __shared__ uint8_t smem_raw[];
