@@ -828,3 +828,43 @@ def test_calib_select_kernel_exact_with_ties(bsfa):
                     assert thr[li, b, h, p] == np.float32(orc.cutoff(desc, kk)), (b, h, p, kk)
                     want_ties[li] += orc.is_tie(desc, kk)
     assert ties.cpu().tolist() == want_ties and sum(want_ties) > 0
+
+
+@pytest.mark.parametrize("hq,hkv,n,causal,heads", [
+    (64, 8, 8192, True, (0, 63)),     # GQA group 8 (Llama-70B layout): four head pairs per kv head
+    (8, 1, 10000, True, (3,)),        # MQA, ragged length (padded to 10112 by repeating the last row)
+    (12, 4, 9000, False, (7,)),       # group 3 (query-block pairs), ragged, non-causal
+])
+def test_other_head_layouts_at_scale(bsfa, hq, hkv, n, causal, heads):
+    """GQA group sizes beyond Llama-8B's and ragged long sequences: mask parity away from T and
+    the output / LSE of sampled heads against the oracle replaying the GPU's decisions."""
+    d, T = 128, 3.84
+    g = hq // hkv
+    gen = torch.Generator(device="cuda").manual_seed(hq * 7 + n)
+    q = torch.randn((1, hq, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tiles = bsfa.TileConfig(128, 64)
+    P = tiles.padded_len(n) // 128
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, hq, P), T, dtype=np.float32), k_levels=(1,),
+                             n_max=tiles.padded_len(n), b_m=128, b_n=64)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True, causal=causal, tiles=tiles)
+    cnt = res.counters.cpu().numpy()
+    assert 0.2 < 1 - cnt[1] / cnt[0] < 0.8
+    for h in heads:
+        qh = q[0, h].float().cpu().numpy()
+        kh = k[0, h // g].float().cpu().numpy()
+        vh = v[0, h // g].float().cpu().numpy()
+        dec = res.decisions[0, h].cpu().numpy()
+        rec = {}
+        o_ref, lse_ref, _ = orc.flash_forward_fast(qh, kh, vh, causal, 128, 64,
+                                                   lambda i_idx, j, sm: dec[i_idx, j] == orc.KEPT, record=rec)
+        for j, (i_idx, smax) in rec.items():
+            far = np.abs(smax - T) > EPS
+            want = np.where(smax > T, orc.KEPT, orc.SKIPPED)
+            assert (dec[i_idx[far], j] == want[far]).all(), (h, j)
+        o_gpu = res.o[0, h].float().cpu().numpy()
+        assert o_gpu.shape == o_ref.shape
+        assert np.abs(o_gpu - o_ref).max() <= ATOL
+        assert _row_rel_err(o_gpu, o_ref) <= ROW_RTOL
+        assert _lse_err(res.lse[0, h].cpu().numpy(), lse_ref) <= LSE_ATOL
