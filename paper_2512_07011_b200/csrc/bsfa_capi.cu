@@ -22,6 +22,14 @@
 #if BSFA_FWD_PAIR
 #include "../../experimental/csrc/bsfa_fwd7.cuh"
 #endif
+// Measurement builds only (-DBSFA_FWD8=1): ThresholdGate at 128x64 on 64-key
+// steps with a per-tile score buffer, experimental/csrc/bsfa_fwd8.cuh
+#ifndef BSFA_FWD8
+#define BSFA_FWD8 0
+#endif
+#if BSFA_FWD8
+#include "../../experimental/csrc/bsfa_fwd8.cuh"
+#endif
 // The round-1 forward and the other measured alternatives live in
 // experimental/csrc (not built); DESIGN.md section 5 has their numbers.
 
@@ -182,6 +190,24 @@ int launch_fwd7(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
 
 #endif
 
+#if BSFA_FWD8
+template <int D>
+int launch_fwd8(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const KernelParams& p, int grid,
+                cudaStream_t st) {
+  using C = FCfg8<D>;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KernelParams) =
+      p.causal ? bsfa_fwd8_kernel<D, true> : bsfa_fwd8_kernel<D, false>;
+  int rc = p.causal ? ensure_smem_attr<bsfa_fwd8_kernel<D, true>>(C::SMEM_BYTES)
+                    : ensure_smem_attr<bsfa_fwd8_kernel<D, false>>(C::SMEM_BYTES);
+  if (rc) return rc;
+  if (grid == 0) return BSFA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(tq, tk, tv, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bsfa forward (v8) launch");
+  return BSFA_OK;
+}
+#endif
+
 int dispatch_fwd(int d, int b_m, int b_n, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                  const KernelParams& p, int grid, cudaStream_t st) {
 #define BSFA_FWD(D_, BM_, BN_) \
@@ -281,8 +307,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
     return rc;
   // (measurement builds) CTA pairs, d = 128, even GQA group: each CTA stages 64 keys of a step
   const bool pair = BSFA_FWD_PAIR && d == 128 && (a->heads_q / a->heads_kv) % 2 == 0;
+  // (measurement builds) v8: ThresholdGate, 128x64 tiles, 64-key K boxes
+  const bool v8 = BSFA_FWD8 && a->gate_mode == BSFA_GATE_THRESHOLD && a->b_m == 128 && a->b_n == 64;
   if (int rc = make_map(&tk, a->k, d, n, a->heads_kv, a->batch, a->k_stride_n, a->k_stride_h, a->k_stride_b,
-                        pair ? 64 : 128, "k"))
+                        (pair || v8) ? 64 : 128, "k"))
     return rc;
   if (int rc =
           make_map(&tv, a->v, d, n, a->heads_kv, a->batch, a->v_stride_n, a->v_stride_h, a->v_stride_b,
@@ -337,6 +365,10 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
   (void)nq;
+#if BSFA_FWD8
+  if (v8) return d == 128 ? launch_fwd8<128>(tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream))
+                          : launch_fwd8<64>(tq, tk, tv, p, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+#endif
 #if BSFA_FWD_PAIR
   if (pair) {
     if (2 * grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
