@@ -868,3 +868,32 @@ def test_other_head_layouts_at_scale(bsfa, hq, hkv, n, causal, heads):
         assert np.abs(o_gpu - o_ref).max() <= ATOL
         assert _row_rel_err(o_gpu, o_ref) <= ROW_RTOL
         assert _lse_err(res.lse[0, h].cpu().numpy(), lse_ref) <= LSE_ATOL
+
+
+def test_plan_replays_in_a_cuda_graph(bsfa):
+    """A BsfaPlan launch (ThresholdGate, GQA) captured in a CUDA graph replays bit for bit, counters
+    included -- the serving loop's launch path (no host work inside the captured region)."""
+    rng = np.random.default_rng(17)
+    B, hq, hkv, n, d = 1, 8, 2, 4096, 128
+    q, k, v = (_dev(rng.standard_normal(s).astype(np.float32))
+               for s in ((B, hq, n, d), (B, hkv, n, d), (B, hkv, n, d)))
+    vals = (3.7 + 0.1 * rng.standard_normal((1, 1, hq, n // 128))).astype(np.float32)
+    t = bsfa.ThresholdTensor(values=vals, k_levels=(3,), n_max=n, b_m=128, b_n=64)
+    plan = bsfa.BsfaPlan(B, hq, hkv, n, d, thresholds=t, k_level=3, return_trace=True)
+    eager = plan.run(q, k, v).clone()
+    dec, cnt, lse = plan.decisions.clone(), plan.counters.clone(), plan.lse.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.run(q, k, v)  # warm-up on the capture stream (kernel attributes, allocator)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        plan.run(q, k, v)
+    plan.o.zero_()
+    plan.decisions.zero_()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(plan.o, eager) and torch.equal(plan.lse, lse) and torch.equal(plan.decisions, dec)
+    assert torch.equal(plan.counters, cnt)
