@@ -76,7 +76,8 @@ typedef struct bsfa_fwd_args {
   int8_t* decisions; /* optional int8 [batch][heads_q][seq_len/b_m][seq_len/b_n]; caller zeroes */
   /* tiles: b_m in {64, 128}, b_n in {64, 128}; seq_len a multiple of 128 (pad
      by repeating the last row); valid_len = unpadded length.  With b_m = 64 the
-     counters count only the reference grid padded to lcm(b_m, b_n). */
+     counters count only the reference grid padded to lcm(b_m, b_n).  head_dim
+     in {64, 128, 256} (zero-pad narrower heads; scale from the original d). */
   unsigned long long* counters; /* optional [4], see BSFA_CNT_* */
   int* status; /* optional; bit 0 set if any row has a non-finite accumulator or l <= 0 */
   /* gate */

@@ -94,8 +94,13 @@ def _check_inputs(q, k, v):
         raise InvalidInputError(f"query heads {hq} must be a multiple of kv heads {hkv}")
     if n < 1 or d < 1:
         raise InvalidInputError("empty sequence or head dimension")
-    if d > 128:
-        raise InvalidInputError(f"head_dim {d} > 128 is not supported by the kernel")
+    if d > 256:
+        raise InvalidInputError(f"head_dim {d} > 256 is not supported by the kernels")
+
+
+def head_dim_pad(d: int) -> int:
+    """The kernels' head_dim for a head of width d: 64, 128 or 256 (zero-padded columns)."""
+    return 64 if d <= 64 else (128 if d <= 128 else 256)
 
 
 def _as_kernel_operand(x: torch.Tensor, n_pad: int, d_pad: int) -> torch.Tensor:
@@ -195,7 +200,7 @@ def _forward(q, k, v, thr_dev, mode: int, window: int, lam: float, *, causal: bo
     thr_positions = int(thr_dev.shape[1]) if thr_dev is not None else 0
     n_pad = tiles.padded_len(n)  # the reference grid
     n_kern = kernel_len(n, tiles)  # n_pad rounded up to the kernels' 128 rows
-    d_pad = 64 if d <= 64 else 128
+    d_pad = head_dim_pad(d)
     sc = reference_scale(d) if scale is None else float(np.float32(scale))
 
     dev = q.device
@@ -317,8 +322,8 @@ class BsfaPlan:
         the threshold comparisons use the padded width's.
         """
         require_kernel_tiles(tiles)
-        if head_dim not in (64, 128):
-            raise InvalidInputError("plans take head_dim 64 or 128 (pad smaller heads and pass their scale)")
+        if head_dim not in (64, 128, 256):
+            raise InvalidInputError("plans take head_dim 64, 128 or 256 (pad smaller heads and pass their scale)")
         if heads_q % heads_kv:
             raise InvalidInputError(f"query heads {heads_q} must be a multiple of kv heads {heads_kv}")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())

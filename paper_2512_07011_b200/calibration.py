@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .attention import reference_scale
+from .attention import head_dim_pad, reference_scale
 from .errors import ConfigurationError, InvalidInputError
 from .thresholds import ThresholdTensor
 from .tiling import TileConfig, kernel_len, off_frontier_count, require_kernel_tiles
@@ -180,7 +180,7 @@ class Calibrator:
         n_kern = kernel_len(n, self.tiles)  # rounded up to the kernel's 128 rows
         if n_pad > self.n_max:
             raise ConfigurationError(f"sample length {n} exceeds calibrator n_max {self.n_max}")
-        d_pad = 64 if self.head_dim <= 64 else 128
+        d_pad = head_dim_pad(self.head_dim)
         qd = _head_operand(q, n_kern, d_pad, self.device)
         kd = _head_operand(k, n_kern, d_pad, self.device)
         if qd.shape[0] != self.num_heads:

@@ -29,15 +29,16 @@ namespace bsfa {
 template <int D, int GT, int BM = 128>
 struct CCfg {
   static constexpr int NCH = D / 64;           // 64-column swizzle atoms along head_dim
+  static constexpr int NQ = D == 256 ? 1 : 2;  // query tiles per CTA (head_dim 256: one)
   static constexpr int Q_TILE = 128 * D * 2;
   static constexpr int K_TILE = 128 * D * 2;   // one 128-key step
-  static constexpr int KS = 3;                 // K ring stages
+  static constexpr int KS = D == 256 ? 2 : 3;  // K ring stages
   static constexpr int MAXA = 4096;            // max off-frontier gate tiles per row
   static constexpr int NBLK = 128 / BM;        // query blocks per 128-row tile
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
-  static constexpr int OFF_CAL = OFF_K + KS * K_TILE;      // int [2 tiles][NBLK][MAXA] ordered maxima
-  static constexpr int OFF_BAR = OFF_CAL + 2 * NBLK * MAXA * 4;
+  static constexpr int OFF_K = OFF_Q + NQ * Q_TILE;
+  static constexpr int OFF_CAL = OFF_K + KS * K_TILE;      // int [NQ tiles][NBLK][MAXA] ordered maxima
+  static constexpr int OFF_BAR = OFF_CAL + NQ * NBLK * MAXA * 4;
   // bar_q, k_full/empty[KS], s_full[2][2 buffers], s_read[2][2 buffers]
   static constexpr int NUM_BARS = 1 + 2 * KS + 4 + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
@@ -85,7 +86,15 @@ __global__ void __launch_bounds__(CCfg<D, GT, BM>::NUM_THREADS, 1)
   int g_;
   {
     const int unit = blockIdx.x;
-    if (p.block_pair) {
+    if constexpr (C::NQ == 1) {
+      // head_dim 256: one query tile per CTA
+      const int per_g = p.num_q_tiles * p.group;
+      g_ = unit / per_g;
+      const int rem = unit - g_ * per_g;
+      qi_a[0] = p.num_q_tiles - 1 - rem / p.group;
+      qi_a[1] = -1;
+      hq_a[0] = hq_a[1] = g_ * p.group + rem % p.group;
+    } else if (p.block_pair) {
       const int per_g = ((p.num_q_tiles + 1) / 2) * p.group;
       g_ = unit / per_g;
       const int rem = unit - g_ * per_g;
@@ -129,7 +138,7 @@ __global__ void __launch_bounds__(CCfg<D, GT, BM>::NUM_THREADS, 1)
     }
     fence_mbarrier_init();
   }
-  for (int i = threadIdx.x; i < 2 * NBLK * C::MAXA; i += blockDim.x) cvals[i] = float_to_ordered(-INFINITY);
+  for (int i = threadIdx.x; i < C::NQ * NBLK * C::MAXA; i += blockDim.x) cvals[i] = float_to_ordered(-INFINITY);
   if (warp == C::MMA_WARP) {
     tmem_alloc(tmem_ptr, C::TMEM_COLS);
     tmem_relinquish();
@@ -147,9 +156,9 @@ __global__ void __launch_bounds__(CCfg<D, GT, BM>::NUM_THREADS, 1)
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_k);
       }
-      mbar_arrive_expect_tx_w(bar_q, 2 * C::Q_TILE);
+      mbar_arrive_expect_tx_w(bar_q, C::NQ * C::Q_TILE);
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+      for (int s = 0; s < C::NQ; ++s)
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
           tma_load_4d_w(sQ + s * C::Q_TILE + c * 128 * 128, &tm_q, bar_q, c * 64, (qi_a[s] < 0 ? 0 : qi_a[s]) * 128,
@@ -178,8 +187,15 @@ __global__ void __launch_bounds__(CCfg<D, GT, BM>::NUM_THREADS, 1)
         const int st = j % KS;
         if (s == 0) mbar_wait(k_full + 8 * st, (j / KS) & 1);
         tc_fence_after();
-        umma_qk_tile_w<D, 128>(tmem + (2 * s + (j & 1)) * 128, dq0 + uint64_t((s * C::Q_TILE) >> 4),
-                               dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
+        if constexpr (D == 256) {  // K = 256: four 64-column atoms, accumulating
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+            umma_qk_chunk_w(tmem + (2 * s + (j & 1)) * 128, dq0 + uint64_t((s * C::Q_TILE + c * 128 * 128) >> 4),
+                            dk0 + uint64_t((st * C::K_TILE + c * 128 * 128) >> 4), IDESC_QK, c > 0 ? 1u : 0u);
+        } else {
+          umma_qk_tile_w<D, 128>(tmem + (2 * s + (j & 1)) * 128, dq0 + uint64_t((s * C::Q_TILE) >> 4),
+                                 dk0 + uint64_t((st * C::K_TILE) >> 4), IDESC_QK);
+        }
         // the stage is released by the last query tile reading it (tile 1 of a
         // block pair stops one step early)
         if (s == (j < ns_a[1] ? 1 : 0)) umma_commit_w(k_empty + 8 * st);

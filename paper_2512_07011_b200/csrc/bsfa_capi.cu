@@ -220,6 +220,10 @@ int dispatch_fwd(int d, int b_m, int b_n, const CUtensorMap& tq, const CUtensorM
   BSFA_FWD(128, 64, 64)
   BSFA_FWD(64, 64, 128)
   BSFA_FWD(128, 64, 128)
+  BSFA_FWD(256, 128, 64)
+  BSFA_FWD(256, 128, 128)
+  BSFA_FWD(256, 64, 64)
+  BSFA_FWD(256, 64, 128)
 #undef BSFA_FWD
   return fail(BSFA_ERR_INVALID, "no kernel for head_dim=%d tiles %dx%d", d, b_m, b_n);
 }
@@ -236,6 +240,10 @@ int dispatch_calib(int d, int b_m, int b_n, const CUtensorMap& tq, const CUtenso
   BSFA_CAL(128, 64, 64)
   BSFA_CAL(64, 64, 128)
   BSFA_CAL(128, 64, 128)
+  BSFA_CAL(256, 128, 64)
+  BSFA_CAL(256, 128, 128)
+  BSFA_CAL(256, 64, 64)
+  BSFA_CAL(256, 64, 128)
 #undef BSFA_CAL
   return fail(BSFA_ERR_INVALID, "no calibration kernel for head_dim=%d tiles %dx%d", d, b_m, b_n);
 }
@@ -285,8 +293,8 @@ int bsfa_debug_trace(long long* dev_buf, int cta) {
 int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   if (!a) return fail(BSFA_ERR_INVALID, "null args");
   if (int rc = check_tiles(a->b_m, a->b_n)) return rc;
-  if (a->head_dim != 64 && a->head_dim != 128)
-    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64 or 128; pad smaller heads)", a->head_dim);
+  if (a->head_dim != 64 && a->head_dim != 128 && a->head_dim != 256)
+    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64, 128 or 256; pad smaller heads)", a->head_dim);
   if (a->batch < 1 || a->heads_q < 1 || a->heads_kv < 1 || a->heads_q % a->heads_kv)
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d batch=%d", a->heads_q, a->heads_kv, a->batch);
   if (a->seq_len < 128 || a->seq_len % 128)
@@ -361,7 +369,9 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
   // query blocks 2m+1 and 2m of one q head (odd groups, MHA included)
   p.block_pair = p.group % 2 == 1 ? 1 : 0;
   const int nq = 2;
-  const long long grid = p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
+  // head_dim 256: one query tile per CTA
+  const long long grid = d == 256 ? (long long)a->batch * a->heads_q * p.num_q_tiles
+                       : p.block_pair ? (long long)a->batch * a->heads_q * ((p.num_q_tiles + 1) / 2)
                                       : (long long)a->batch * (a->heads_q / nq) * p.num_q_tiles;
   if (grid > 0x7fffffffLL) return fail(BSFA_ERR_INVALID, "grid too large");
   (void)nq;
@@ -382,8 +392,8 @@ int bsfa_fwd(const bsfa_fwd_args* a, void* stream) {
 int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   if (!a) return fail(BSFA_ERR_INVALID, "null args");
   if (int rc = check_tiles(a->b_m, a->b_n)) return rc;
-  if (a->head_dim != 64 && a->head_dim != 128)
-    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64 or 128; pad smaller heads)", a->head_dim);
+  if (a->head_dim != 64 && a->head_dim != 128 && a->head_dim != 256)
+    return fail(BSFA_ERR_INVALID, "head_dim %d unsupported (64, 128 or 256; pad smaller heads)", a->head_dim);
   if (a->heads_q < 1 || a->heads_kv < 1 || a->heads_q % a->heads_kv)
     return fail(BSFA_ERR_INVALID, "bad head counts q=%d kv=%d", a->heads_q, a->heads_kv);
   if (a->seq_len < 128 || a->seq_len % 128)
@@ -440,7 +450,9 @@ int bsfa_calib_blockmax(const bsfa_calib_args* a, void* stream) {
   // odd groups (MHA included): two query blocks of one head per CTA, as in the forward
   p.block_pair = p.group % 2 == 1 ? 1 : 0;
   const int nq = 2;
-  const int grid = p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2) : (a->heads_q / nq) * p.num_q_tiles;
+  const int grid = d == 256       ? a->heads_q * p.num_q_tiles  // one query tile per CTA
+                   : p.block_pair ? a->heads_q * ((p.num_q_tiles + 1) / 2)
+                                  : (a->heads_q / nq) * p.num_q_tiles;
   (void)nq;
   return dispatch_calib(d, a->b_m, a->b_n, tq, tk, p, grid, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -94,8 +94,13 @@ namespace bsfa {
 // chunks = 3 steps) beats a deeper V ring (BSFA 1.1 % faster at 32K, 0.5 % at
 // 128K); the statically gated ones (dense, frontier, window) prefetch V and
 // keep the 6-unit V ring (dense 1.1-1.4 % faster with it).
+// head_dim 256: ONE query tile per CTA whose O spans both O slots of the
+// D = 128 layout (O 256 columns | S 128 | P 64 = 448 of 512), QK with K = 256
+// and one N = 256 PV per 64-key unit; rings 6 K chunks (1.5 steps) + 2 V
+// units (one step) so Q + K + V fit in 224 KB.
 template <int D, int GT, int GM = 1>
 struct FCfg3 {
+  static constexpr int NQ = D == 256 ? 1 : 2;   // query tiles per CTA
   static constexpr int BN = 128 / GT;           // gate tile width (reference b_n)
   static constexpr int NCH = D / 64;            // 64-column swizzle atoms along head_dim
   static constexpr int Q_TILE = 128 * D * 2;
@@ -103,11 +108,11 @@ struct FCfg3 {
   static constexpr int K_CHUNK = 128 * 128;     // 128 keys x 64 columns, bf16
   static constexpr int V_UNIT = 64 * D * 2;     // 64 keys of V
   static constexpr int V_ATOM = 64 * 128;       // 64 keys x 64 columns
-  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : (GM == 1 ? 4 : 6);
-  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 128 ? (GM == 1 ? 6 : 4) : 8);
+  static constexpr int KC = BSFA_FWD3_KC ? BSFA_FWD3_KC : (D == 256 ? 6 : (GM == 1 ? 4 : 6));
+  static constexpr int VS = BSFA_FWD3_VS ? BSFA_FWD3_VS : (D == 256 ? 2 : (D == 128 ? (GM == 1 ? 6 : 4) : 8));
   static constexpr int DQ = 8;                  // decision ring depth (V producer)
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
+  static constexpr int OFF_K = OFF_Q + NQ * Q_TILE;
   static constexpr int OFF_V = OFF_K + KC * K_CHUNK;
   static constexpr int OFF_BAR = OFF_V + VS * V_UNIT;
   // bar_q, k_full/empty[KC], v_full/empty[VS], s_full[2], s_free,
@@ -120,7 +125,7 @@ struct FCfg3 {
   static constexpr int OFF_TMEMPTR = OFF_VOTE + 2 * 2 * 4 * 4;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   static constexpr int O_COL = 0;          // O_s at s * D
-  static constexpr int S_COL = 2 * D;      // the shared score buffer
+  static constexpr int S_COL = NQ * D;     // the shared score buffer
   static constexpr int P_COL = S_COL + 128;  // P_s (bf16 pairs) at P_COL + s * 64
   static constexpr int TMEM_COLS = 512;
   static constexpr int NUM_THREADS = 12 * 32;
@@ -129,7 +134,7 @@ struct FCfg3 {
   static constexpr int REG_LAUNCH = (65536 / NUM_THREADS) / 8 * 8;                       // 168
   static constexpr int REG_SOFT = (NUM_THREADS * REG_LAUNCH - 128 * REG_OTHER) / 256 / 8 * 8;  // 224
   static_assert(GT == 1 || GT == 2, "b_n in {64, 128}");
-  static_assert(D == 64 || D == 128, "head_dim 64 or 128");
+  static_assert(D == 64 || D == 128 || D == 256, "head_dim 64, 128 or 256");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(P_COL + 128 <= TMEM_COLS, "TMEM budget");
   static_assert(KC >= NCH + 1 || KC >= 2, "K ring");
@@ -188,7 +193,18 @@ __global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
   int b_, g_, qi_;
   {
     const int unit = blockIdx.x;
-    if (p.block_pair) {
+    if constexpr (C::NQ == 1) {
+      // head_dim 256: one query tile per CTA, (batch, kv head) major, heaviest block first
+      const int per_bg = p.num_q_tiles * p.group;
+      const int bg = unit / per_bg;
+      const int rem = unit - bg * per_bg;
+      b_ = bg / p.heads_kv;
+      g_ = bg - b_ * p.heads_kv;
+      qi_ = p.num_q_tiles - 1 - rem / p.group;
+      qi_a[0] = qi_;
+      qi_a[1] = -1;  // no second tile
+      hq_a[0] = hq_a[1] = g_ * p.group + rem % p.group;
+    } else if (p.block_pair) {
       const int per_bg = ((p.num_q_tiles + 1) / 2) * p.group;
       const int bg = unit / per_bg;
       const int rem = unit - bg * per_bg;
@@ -291,9 +307,9 @@ __global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_k);
       }
-      mbar_arrive_expect_tx_w(bar_q, 2 * C::Q_TILE);
+      mbar_arrive_expect_tx_w(bar_q, C::NQ * C::Q_TILE);
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+      for (int s = 0; s < C::NQ; ++s)
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
           tma_load_4d_w(sQ + s * C::Q_TILE + c * C::Q_ATOM, &tm_q, bar_q, c * 64, (qi_a[s] < 0 ? 0 : qi_a[s]) * 128,
