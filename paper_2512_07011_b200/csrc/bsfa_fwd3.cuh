@@ -455,10 +455,12 @@ __global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
           if (NCH == 2 && wait_s)
             mbar_wait3(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1,
                        k_full + 8 * int((u0 + 1) % KC), ((u0 + 1) / KC) & 1);
-          else if (wait_s)
+          else if (NCH == 1 && wait_s)
             mbar_wait2(s_free, sfree_ph & 1u, k_full + 8 * int(u0 % KC), (u0 / KC) & 1);
-          else
+          else {  // (head_dim 256: four chunks)
+            if (wait_s) mbar_wait(s_free, sfree_ph & 1u);
             for (int c = 0; c < NCH; ++c) mbar_wait(k_full + 8 * int((u0 + c) % KC), ((u0 + c) / KC) & 1);
+          }
         } else {
           mbar_wait(s_free, sfree_ph & 1u);
         }

@@ -148,3 +148,31 @@ def test_d256_calibration_matches_oracle(bsfa, d, b_m):
     np.testing.assert_array_equal(t.values[~fin], ref[~fin])
     assert np.abs(t.values[fin] - ref[fin]).max() <= 1e-4
     assert {kk: t.diagnostics.tie_counts[kk] for kk in levels} == {kk: int(ties[kk]) for kk in levels}
+
+
+@pytest.mark.parametrize("T", [3.9, 9.0])
+def test_d256_at_scale_sampled_heads(bsfa, T):
+    """16 q / 8 kv heads x 16K tokens at d = 256 (Gemma-like), ~40 % kept and frontier-only-like
+    thresholds: mask parity away from T and output / LSE parity of sampled heads against the oracle
+    replaying the GPU's decisions (the regime where K chunks stream while the MMAs run)."""
+    n, d, hq, hkv = 16384, 256, 16, 8
+    gen = torch.Generator(device="cuda").manual_seed(5 + int(T))
+    q = torch.randn((1, hq, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, hkv, n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    t = bsfa.ThresholdTensor(values=np.full((1, 1, hq, n // 128), T, dtype=np.float32), k_levels=(1,),
+                             n_max=n, b_m=128, b_n=64)
+    res = bsfa.attention(q, k, v, thresholds=t, k_level=1, return_trace=True)
+    for h in (0, 13):
+        qh, kh, vh = (x[0, hh].float().cpu().numpy() for x, hh in ((q, h), (k, h // 2), (v, h // 2)))
+        dec = res.decisions[0, h].cpu().numpy()
+        rec = {}
+        o_ref, lse_ref, _ = orc.flash_forward_fast(qh, kh, vh, True, 128, 64,
+                                                   lambda i_idx, j, sm: dec[i_idx, j] == orc.KEPT, record=rec)
+        for j, (i_idx, smax) in rec.items():
+            far = np.abs(smax - T) > EPS
+            want = np.where(smax > T, orc.KEPT, orc.SKIPPED)
+            assert (dec[i_idx[far], j] == want[far]).all(), (h, j)
+        o_gpu = res.o[0, h].float().cpu().numpy()
+        assert np.abs(o_gpu - o_ref).max() <= ATOL and _row_rel_err(o_gpu, o_ref) <= ROW_RTOL
+        assert _lse_err(res.lse[0, h].cpu().numpy(), lse_ref) <= LSE_ATOL

@@ -20,18 +20,22 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--gate", default="threshold")
 ap.add_argument("--T", type=float, default=3.84)
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--heads-q", type=int, default=32)
+ap.add_argument("--heads-kv", type=int, default=8)
+ap.add_argument("--head-dim", type=int, default=128)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
-cfg = dict(heads_q=32, heads_kv=8, seq_len=a.seq, head_dim=128)
+cfg = dict(heads_q=a.heads_q, heads_kv=a.heads_kv, seq_len=a.seq, head_dim=a.head_dim)
 q, k, v = bench.make_inputs(cfg, 0, dev)
 tiles = bsfa.TileConfig(128, 64)
 thr = None
 if a.gate == "threshold":
     P = a.seq // 128
-    thr = bsfa.ThresholdTensor(values=np.full((1, 1, 32, P), a.T, dtype=np.float32), k_levels=(1,), n_max=a.seq,
-                               b_m=128, b_n=64)
-plan = bsfa.BsfaPlan(1, 32, 8, a.seq, 128, tiles=tiles, thresholds=thr, k_level=1 if thr else None, device=dev)
+    thr = bsfa.ThresholdTensor(values=np.full((1, 1, a.heads_q, P), a.T, dtype=np.float32), k_levels=(1,),
+                               n_max=a.seq, b_m=128, b_n=64)
+plan = bsfa.BsfaPlan(1, a.heads_q, a.heads_kv, a.seq, a.head_dim, tiles=tiles, thresholds=thr,
+                     k_level=1 if thr else None, device=dev)
 for _ in range(a.launches):
     plan.run(q, k, v)
 torch.cuda.synchronize()
