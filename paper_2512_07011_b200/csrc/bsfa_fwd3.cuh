@@ -79,6 +79,12 @@
 #ifndef BSFA_SFREE_NB
 #define BSFA_SFREE_NB 2
 #endif
+// b_n = 128 ThresholdGate through the vote words + V producer in the barrier
+// (as b_n = 64) instead of BAR.RED.OR + the decision ring: 128x128 BSFA 15 %
+// faster at 32K, 10 % at 128K (profiles/r02_s3_ab_gt1vp.jsonl)
+#ifndef BSFA_VOTE1_GT1
+#define BSFA_VOTE1_GT1 1
+#endif
 #ifndef BSFA_MAXTREE
 #define BSFA_MAXTREE 0
 #endif
@@ -253,7 +259,8 @@ __global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
   };
   // statically known decision bits of step j for query block qi (-1: voted)
   // the V producer reads ThresholdGate decisions straight from the vote words
-  constexpr bool VP = GM == 0 && (GT == 2 || BM == 64) && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
+  // (BSFA_VOTE1_GT1 = 0: b_n = 128 keeps the BAR.RED.OR vote and the decision ring)
+  constexpr bool VP = GM == 0 && (GT == 2 || BM == 64 || BSFA_VOTE1_GT1) && BSFA_VOTE1 && BSFA_VOTE_PRODUCER;
   constexpr bool SNB = !BSFA_FWD3_SPLIT && (BSFA_SFREE_NB == 1 || (BSFA_SFREE_NB == 2 && GM == 1));
   auto sbits = [&](int j, int qi) -> int {
     if constexpr (GM == 1) return step_static_bits<GT>(gate_mode, window, j, qi);
@@ -720,12 +727,14 @@ __global__ void __launch_bounds__(FCfg3<D, GT, GM>::NUM_THREADS, 1)
           bits = uint32_t(sb);
         } else if constexpr (GM == 0) {
           // ThresholdGate: keep iff tile max (scaled) > T (gates.py:77-78)
-          if constexpr (GT == 2 && BSFA_VOTE1) {
+          if constexpr ((GT == 2 || BSFA_VOTE1_GT1) && BSFA_VOTE1) {
             // both gate tiles in ONE barrier: OR within the warp (REDUX), one word
             // per warp in shared memory (parity double-buffered: a warp reaches
             // step j+2's store only after every warp passed step j+1's barrier,
             // i.e. read step j's words), bar.sync, OR of the four words
-            const uint32_t v = (mx[0] * scale > T ? 1u : 0u) | (mx[1] * scale > T ? 2u : 0u);
+            uint32_t v = 0;
+#pragma unroll
+            for (int x = 0; x < GT; ++x) v |= (mx[x] * scale > T ? 1u : 0u) << x;
             const uint32_t wv = __reduce_or_sync(0xffffffffu, v);
             const uint32_t slot = vote_sm + (s * 2 + (j & 1)) * 16;
             if (lane == 0) sts_u32(slot + wq * 4, wv);

@@ -29,10 +29,11 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--density", type=float, default=0.5)
 ap.add_argument("--rounds", type=int, default=8)
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--tiles", default="128x64", help="b_m x b_n")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
-tiles = bsfa.TileConfig(128, 64)
+tiles = bsfa.TileConfig(*(int(x) for x in a.tiles.split("x")))
 cfg = dict(heads_q=32, heads_kv=8, seq_len=a.seq, head_dim=128)
 kl = costs.k_for_density(a.seq, tiles, a.density)
 thr = bench.calibrated_thresholds(cfg, tiles, kl, dev)
