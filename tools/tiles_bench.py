@@ -30,6 +30,7 @@ ap.add_argument("--tiles", nargs="+", default=["128x64", "128x128", "64x64", "64
 ap.add_argument("--heads-q", type=int, default=32)
 ap.add_argument("--heads-kv", type=int, default=8)
 ap.add_argument("--head-dim", type=int, default=128)
+ap.add_argument("--non-causal", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
@@ -42,8 +43,9 @@ for spec in a.tiles:
     kl = costs.k_for_density(a.seq, tiles, a.density)
     thr = bench.calibrated_thresholds(cfg, tiles, kl, dev)
     hq, hkv, d = a.heads_q, a.heads_kv, a.head_dim
-    pb = bsfa.BsfaPlan(1, hq, hkv, a.seq, d, tiles=tiles, thresholds=thr, k_level=kl, device=dev)
-    pd = bsfa.BsfaPlan(1, hq, hkv, a.seq, d, tiles=tiles, device=dev)
+    causal = not a.non_causal
+    pb = bsfa.BsfaPlan(1, hq, hkv, a.seq, d, tiles=tiles, thresholds=thr, k_level=kl, device=dev, causal=causal)
+    pd = bsfa.BsfaPlan(1, hq, hkv, a.seq, d, tiles=tiles, device=dev, causal=causal)
     for p in (pb, pd):
         p.run(q, k, v)
     torch.cuda.synchronize()
@@ -55,7 +57,8 @@ for spec in a.tiles:
             res[arm].append(t / 3)
     mb, md = statistics.median(res["bsfa"]), statistics.median(res["dense"])
     f_exec = costs.executed_flops(cnt[0], cnt[1], tiles, d)
-    print(json.dumps({"tiles": spec, "seq": a.seq, "heads": [hq, hkv], "head_dim": d, "k_level": kl,
+    print(json.dumps({"tiles": spec, "seq": a.seq, "causal": causal, "heads": [hq, hkv], "head_dim": d,
+                      "k_level": kl,
                       "predicted_density": round(costs.predicted_density(a.seq, tiles, kl), 4),
                       "measured_density": round(cnt[1] / cnt[0], 4),
                       "v_units_skipped_frac": round(1 - cnt[2] / cnt[3], 4),
