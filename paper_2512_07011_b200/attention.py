@@ -11,7 +11,11 @@
 
 Semantics kept from the reference engine:
   - sequences are padded to lcm(b_m, b_n) by repeating the last row
-    (engine.py:99-114) and outputs sliced back to the valid length;
+    (engine.py:99-114), then to the kernels' 128-row tiles
+    (``tiling.kernel_len``), and outputs / the trace are sliced back to the
+    valid length / the reference grid;
+  - head_dim d <= 256 is zero-padded to 64, 128 or 256 columns with the
+    scale of the original d;
   - frontier tiles are always processed with the element-wise causal mask,
     off-frontier tiles go through the gate (engine.py:157-175);
   - keep iff max(QK^T * scale over the tile) > T, strictly (gates.py:77-78);
