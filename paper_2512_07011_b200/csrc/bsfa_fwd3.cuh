@@ -26,6 +26,11 @@
 // Shared memory: Q 2 x 128 rows x D, K ring of KC 64-column chunks (128 keys),
 // V ring of VS units of 64 keys x D (one unit per kept 64-key half).
 //
+// head_dim 256 (FCfg3::NQ = 1): one query tile per CTA, its O spanning both O
+// slots (O 256 | S 128 | P 64 columns), tile 1 absent (qi = -1, as for the
+// missing second block of an odd block pair).  b_m = 64 (BM): see the
+// template comment below.
+//
 // Warp roles (384 threads):
 //   warps 0-3 / 4-7  softmax of query tile 0 / 1, thread r owns row r (TMEM lane r)
 //   warp 8           TMA: Q once, K chunks
@@ -33,7 +38,9 @@
 //   warp 10          TMA: V units, fetched only when some query tile kept them
 //   warp 11          idle (completes the warpgroup for setmaxnreg)
 // Per step and tile: QK = D/16 MMAs 128x128x16 (SS, K-major SW128); gate vote
-// rowmax*scale > T OR-reduced over the 128 rows by BAR.RED.OR (gates.py:77-78);
+// rowmax*scale > T OR-reduced over the 128 rows (gates.py:77-78: warp REDUX +
+// shared vote words + a named barrier the V producer joins; RunningMaxGate:
+// BAR.RED.OR per gate tile);
 // skipped gate tiles get no V TMA, no exponentials, no PV (engine.py:172-174);
 // kept ones run the lazily rescaled online softmax (engine.py:57-68) and
 // O_s += P_h V_h as 4 MMAs 128xDx16 (TS: P from TMEM, V MN-major SW128) per
